@@ -1,0 +1,82 @@
+// Shared helpers for the pf_b200 kernels: status plumbing, launch accounting,
+// pyramid addressing and the reference's rounding rules.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/pf_b200.h"
+
+namespace pf {
+
+// Thread-local last error; set by every failing entry point.
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int check_cuda(cudaError_t err, const char* what);
+void count_launch();
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Launch-check helper used right after every <<<>>>.
+inline int after_launch(const char* what) {
+    count_launch();
+    return check_cuda(cudaGetLastError(), what);
+}
+
+// round_half_away for x >= 0 (pkg/store.py:70-72): floor(x + 0.5).
+__host__ __device__ inline int64_t rha_nonneg(double x) {
+#ifdef __CUDA_ARCH__
+    return (int64_t)floor(__dadd_rn(x, 0.5));
+#else
+    return (int64_t)floor(x + 0.5);
+#endif
+}
+
+// Address of pixel (X, Y) in a padded tile-major level (see pf_b200.h).
+__device__ __forceinline__ const uint8_t* level_pixel(const pf_slide_desc& s, int level, int X,
+                                                      int Y) {
+    const int T = s.tile_size;
+    const int tx = X / T, ty = Y / T;
+    const int u = X - tx * T, v = Y - ty * T;
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(s.level_ptr[level]);
+    const size_t tile_bytes = (size_t)T * T * 3;
+    return base + ((size_t)ty * s.tiles_x[level] + tx) * tile_bytes + ((size_t)v * T + u) * 3;
+}
+
+__device__ __forceinline__ uint8_t* level_pixel_mut(const pf_slide_desc& s, int level, int X,
+                                                    int Y) {
+    return const_cast<uint8_t*>(level_pixel(s, level, X, Y));
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// SplitMix64 finaliser (pkg/rng.py:25-30).
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// Draw `counter` (1-based) of a stream with key `key` (pkg/rng.py:60-62).
+__host__ __device__ __forceinline__ uint64_t stream_u64(uint64_t key, uint64_t counter) {
+    return mix64(key + counter * 0x9E3779B97F4A7C15ull);
+}
+
+// RandomStream.uniform(0, 1) (pkg/rng.py:64-67): (u >> 11) * 2^-53, exact.
+__host__ __device__ __forceinline__ double u64_to_unit(uint64_t u) {
+    return (double)(u >> 11) * 1.1102230246251565e-16;  // 2^-53
+}
+
+// randrange limit (pkg/rng.py:69-77): floor(2^64 / n) * n; returns 0 to mean 2^64.
+__host__ __device__ __forceinline__ uint64_t randrange_limit(uint64_t n) {
+    // 2^64 mod n == (2^64 - n) mod n
+    const uint64_t rem = (0ull - n) % n;
+    return 0ull - rem;  // 2^64 - rem, wraps to 0 when rem == 0
+}
+__host__ __device__ __forceinline__ bool randrange_accepts(uint64_t v, uint64_t limit) {
+    return limit == 0ull || v < limit;
+}
+
+}  // namespace pf

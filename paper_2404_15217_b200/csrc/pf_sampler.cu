@@ -1,0 +1,413 @@
+// Batched overlap_fraction and the epoch_stream sampler.
+//
+// epoch_stream (pkg/sampler.py:196-227) is sequential: a slide draw, then up
+// to max_attempts candidates of sample_patch (140-184), each consuming one
+// mpp draw and - when the footprint fits - two coordinate draws, until one is
+// accepted by overlap_fraction >= min_foreground.  All draws come from
+// counter-based SplitMix64 streams (pkg/rng.py), so when every (slide, mpp)
+// footprint fits and no randrange rejection occurs, candidate number m of the
+// stream on slide s is a pure function of (s, m):
+//     mpp draw m+1, coords draws 2m+1, 2m+2.
+// The sampler therefore (1) evaluates the acceptance bit A(s, m) of every
+// slide for a window of attempts in parallel — one warp per candidate, FP64
+// overlap test bit-exact with the reference — and (2) walks the slide draws in
+// stream order with a single warp, taking for each draw the first accepted
+// attempt within its max_attempts budget (an ordered compaction of the accept
+// bitmaps via find-first-set).  Exhausted draws consume max_attempts attempts
+// and no sequence number, exactly like the reference.  Whenever the
+// assumptions do not hold (a footprint that does not fit, a rejected draw,
+// a window that ran out) the walk continues on the sequential exact path.
+#include "pf_common.cuh"
+#include "pf_poly.cuh"
+
+namespace pf {
+
+// ---------------------------------------------------------------------------
+// pf_overlap_fraction: one warp per rect.
+// ---------------------------------------------------------------------------
+__global__ void overlap_kernel(const void* blob, const double* rects, int n, int grid, double* out) {
+    extern __shared__ __align__(16) uint32_t s_masks[];
+    const int warp_in_block = threadIdx.x >> 5;
+    const int q = blockIdx.x * (blockDim.x >> 5) + warp_in_block;
+    if (q >= n) return;
+    const PolyView P = poly_view(blob);
+    uint32_t* sm = s_masks + warp_in_block * (overlap_smem_bytes(grid) / 4);
+    const double x = rects[4 * q], y = rects[4 * q + 1], w = rects[4 * q + 2], h = rects[4 * q + 3];
+    const int c = warp_overlap_count(P, x, y, w, h, grid, sm);
+    if ((threadIdx.x & 31) == 0) out[q] = c < 0 ? 0.0 : __ddiv_rn((double)c, (double)grid * (double)grid);
+}
+
+// ---------------------------------------------------------------------------
+// Sampler helpers (pkg/rng.py, pkg/sampler.py)
+// ---------------------------------------------------------------------------
+struct SamplerWs {
+    uint32_t* bitmaps;  // [n_slides][window/32]
+    int4* cands;        // [n_slides][window]: x, y, mpp_idx, -
+    int32_t* reject_at; // first window offset whose coords draws were rejected
+};
+
+__host__ __device__ inline SamplerWs carve_ws(void* ws, int n_slides, int window) {
+    SamplerWs w;
+    uint8_t* p = reinterpret_cast<uint8_t*>(ws);
+    w.reject_at = reinterpret_cast<int32_t*>(p);
+    p += 256;
+    w.bitmaps = reinterpret_cast<uint32_t*>(p);
+    p += (((size_t)n_slides * (window / 32) * 4) + 255) / 256 * 256;
+    w.cands = reinterpret_cast<int4*>(p);
+    return w;
+}
+
+__host__ __device__ inline int64_t ws_bytes(int n_slides, int window) {
+    return 256 + ((int64_t)n_slides * (window / 32) * 4 + 255) / 256 * 256 +
+           (int64_t)n_slides * window * 16;
+}
+
+// RandomStream.weighted_index (rng.py:88-103) given the stream draw u.
+__device__ __forceinline__ int weighted_pick(uint64_t u, const double* w, int n) {
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) total = __dadd_rn(total, w[i]);
+    const double v = __dadd_rn(0.0, __dmul_rn(u64_to_unit(u), __dsub_rn(total, 0.0)));
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) {
+        acc = __dadd_rn(acc, w[i]);
+        if (v < acc) return i;
+    }
+    return n - 1;
+}
+
+__device__ __forceinline__ void emit_spec(const pf_sampler_config& cfg, const pf_sampler_slide& sl,
+                                          const pf_slide_desc& sd, int s, int x, int y, int mi,
+                                          int64_t seq, pf_patch_spec* out) {
+    pf_patch_spec sp;
+    sp.seq = seq;
+    sp.target_mpp = cfg.mpp[mi];
+    sp.slide = s;
+    sp.x = x;
+    sp.y = y;
+    sp.width = sl.fp[mi];
+    sp.height = sl.fp[mi];
+    sp.out_size = cfg.patch_size;
+    sp.mpp_idx = mi;
+    sp.level = sl.level[mi];
+    sp.side = sl.side[mi];
+    const double ds = (double)sd.downsample[sp.level];
+    sp.sx = (int32_t)floor(__dadd_rn(__ddiv_rn((double)x, ds), 0.5));
+    sp.sy = (int32_t)floor(__dadd_rn(__ddiv_rn((double)y, ds), 0.5));
+    sp.flags = 0;
+    *out = sp;
+}
+
+// ---------------------------------------------------------------------------
+// Speculative evaluation: one warp per (slide, window offset).
+// ---------------------------------------------------------------------------
+__global__ void sample_eval_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
+                                   const pf_sampler_state* state, SamplerWs ws, int window, int n) {
+    extern __shared__ __align__(16) uint32_t s_masks[];
+    if (state->status != PF_OK || state->emitted >= n) return;
+    const int warp_in_block = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_in_block;
+    if (q >= (int64_t)cfg.n_slides * window) return;
+    const int s = (int)(q / window), a = (int)(q % window);
+    const pf_sampler_slide& sl = slides[s];
+    const uint64_t m0 = state->c_mpp, c0 = state->c_coords;
+    const int mi = weighted_pick(stream_u64(cfg.key_mpp, m0 + (uint64_t)a + 1), cfg.mpp_weight, cfg.n_mpps);
+    const int fp = sl.fp[mi];
+    const uint64_t nx = (uint64_t)(sl.x_hi[mi] - sl.x_lo[mi] + 1);
+    const uint64_t ny = (uint64_t)(sl.y_hi[mi] - sl.y_lo[mi] + 1);
+    const uint64_t vx = stream_u64(cfg.key_coords, c0 + 2ull * (uint64_t)a + 1);
+    const uint64_t vy = stream_u64(cfg.key_coords, c0 + 2ull * (uint64_t)a + 2);
+    const bool rejected = !randrange_accepts(vx, randrange_limit(nx)) || !randrange_accepts(vy, randrange_limit(ny));
+    if (rejected) {
+        if (lane == 0) atomicMin(ws.reject_at, a);
+        return;
+    }
+    const int x = sl.x_lo[mi] + (int)(vx % nx);
+    const int y = sl.y_lo[mi] + (int)(vy % ny);
+    const PolyView P = poly_view(reinterpret_cast<const void*>(sl.poly_blob));
+    uint32_t* sm = s_masks + warp_in_block * (overlap_smem_bytes(cfg.grid) / 4);
+    const int c = warp_overlap_count(P, (double)x, (double)y, (double)fp, (double)fp, cfg.grid, sm);
+    const double frac = c < 0 ? 0.0 : __ddiv_rn((double)c, (double)cfg.grid * (double)cfg.grid);
+    if (lane == 0) {
+        ws.cands[(size_t)s * window + a] = make_int4(x, y, mi, 0);
+        if (frac >= cfg.min_foreground)
+            atomicOr(ws.bitmaps + (size_t)s * (window / 32) + (a >> 5), 1u << (a & 31));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Ordered walk (single warp).  Lane 0 drives; lanes help with slide draws.
+// ---------------------------------------------------------------------------
+struct WalkState {
+    uint64_t c_slide, c_coords, c_mpp;
+    int64_t seq, failures, attempts, slow;
+    int32_t emitted, cur_slide, cur_used, status;
+};
+
+__device__ inline void load_ws(const pf_sampler_state* st, WalkState& w) {
+    w.c_slide = st->c_slide;
+    w.c_coords = st->c_coords;
+    w.c_mpp = st->c_mpp;
+    w.seq = st->seq;
+    w.failures = st->consecutive_failures;
+    w.attempts = st->attempts;
+    w.slow = st->slow_evals;
+    w.emitted = st->emitted;
+    w.cur_slide = st->cur_slide;
+    w.cur_used = st->cur_used;
+    w.status = st->status;
+}
+
+__device__ inline void store_ws(pf_sampler_state* st, const WalkState& w) {
+    st->c_slide = w.c_slide;
+    st->c_coords = w.c_coords;
+    st->c_mpp = w.c_mpp;
+    st->seq = w.seq;
+    st->consecutive_failures = w.failures;
+    st->attempts = w.attempts;
+    st->slow_evals = w.slow;
+    st->emitted = w.emitted;
+    st->cur_slide = w.cur_slide;
+    st->cur_used = w.cur_used;
+    st->status = w.status;
+}
+
+// sample_slide (sampler.py:130-137): one call = one randrange / weighted_index.
+__device__ inline int draw_slide(const pf_sampler_config& cfg, const pf_sampler_slide* slides,
+                                 uint64_t& c_slide) {
+    if (cfg.strategy == 0) {
+        const uint64_t n = (uint64_t)cfg.n_slides;
+        const uint64_t lim = randrange_limit(n);
+        while (true) {
+            const uint64_t v = stream_u64(cfg.key_slide, ++c_slide);
+            if (randrange_accepts(v, lim)) return (int)(v % n);
+        }
+    }
+    const uint64_t u = stream_u64(cfg.key_slide, ++c_slide);
+    double total = 0.0;
+    for (int i = 0; i < cfg.n_slides; ++i) total = __dadd_rn(total, slides[i].weight);
+    const double v = __dadd_rn(0.0, __dmul_rn(u64_to_unit(u), __dsub_rn(total, 0.0)));
+    double acc = 0.0;
+    for (int i = 0; i < cfg.n_slides; ++i) {
+        acc = __dadd_rn(acc, slides[i].weight);
+        if (v < acc) return i;
+    }
+    return cfg.n_slides - 1;
+}
+
+__device__ inline int64_t failure_limit(const pf_sampler_config& cfg) {
+    return max((int64_t)100, (int64_t)10 * cfg.n_slides);
+}
+
+// One exact attempt of sample_patch on the current slide (warp-wide).
+// Returns 1 if a spec was emitted.
+__device__ inline int slow_attempt(const pf_sampler_config& cfg, const pf_sampler_slide* slides,
+                                   const pf_slide_desc* descs, WalkState& w, pf_patch_spec* out,
+                                   uint32_t* sm) {
+    const int s = w.cur_slide;
+    const pf_sampler_slide& sl = slides[s];
+    const int mi = weighted_pick(stream_u64(cfg.key_mpp, ++w.c_mpp), cfg.mpp_weight, cfg.n_mpps);
+    w.cur_used += 1;
+    w.attempts += 1;
+    if (sl.x_hi[mi] < sl.x_lo[mi] || sl.y_hi[mi] < sl.y_lo[mi]) return 0;  // no coords draw
+    const uint64_t nx = (uint64_t)(sl.x_hi[mi] - sl.x_lo[mi] + 1);
+    const uint64_t ny = (uint64_t)(sl.y_hi[mi] - sl.y_lo[mi] + 1);
+    uint64_t v;
+    do { v = stream_u64(cfg.key_coords, ++w.c_coords); } while (!randrange_accepts(v, randrange_limit(nx)));
+    const int x = sl.x_lo[mi] + (int)(v % nx);
+    do { v = stream_u64(cfg.key_coords, ++w.c_coords); } while (!randrange_accepts(v, randrange_limit(ny)));
+    const int y = sl.y_lo[mi] + (int)(v % ny);
+    const PolyView P = poly_view(reinterpret_cast<const void*>(sl.poly_blob));
+    const int fp = sl.fp[mi];
+    const int c = warp_overlap_count(P, (double)x, (double)y, (double)fp, (double)fp, cfg.grid, sm);
+    w.slow += 1;
+    const double frac = c < 0 ? 0.0 : __ddiv_rn((double)c, (double)cfg.grid * (double)cfg.grid);
+    if (frac >= cfg.min_foreground) {
+        if ((threadIdx.x & 31) == 0) emit_spec(cfg, sl, descs[s], s, x, y, mi, w.seq, out + w.emitted);
+        w.seq += 1;
+        w.emitted += 1;
+        w.failures = 0;
+        w.cur_slide = -1;
+        return 1;
+    }
+    return 0;
+}
+
+__global__ void sample_walk_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
+                                   const pf_slide_desc* descs, pf_sampler_state* state, SamplerWs ws,
+                                   int window, int n, int use_table, int finish, pf_patch_spec* out) {
+    extern __shared__ __align__(16) uint32_t s_masks[];
+    WalkState w;
+    load_ws(state, w);
+    if (w.status != PF_OK || w.emitted >= n) return;
+    const int lane = threadIdx.x & 31;
+    const int max_att = cfg.max_attempts;
+    const int64_t flimit = failure_limit(cfg);
+    if (use_table) {
+        const uint64_t m0 = w.c_mpp, c0 = w.c_coords;
+        const int wlim = min(window, *ws.reject_at);
+        const int words = window / 32;
+        while (w.emitted < n && w.status == PF_OK) {
+            if (w.cur_slide < 0) {
+                w.cur_slide = draw_slide(cfg, slides, w.c_slide);
+                w.cur_used = 0;
+            }
+            const int a0 = (int)(w.c_mpp - m0);
+            const int budget = max_att - w.cur_used;
+            const int avail = wlim - a0;
+            const int span = min(budget, avail);
+            // first accepted attempt of slide cur_slide in [a0, a0 + span)
+            int found = -1;
+            if (span > 0) {
+                const uint32_t* bm = ws.bitmaps + (size_t)w.cur_slide * words;
+                const int wfirst = a0 >> 5, wlast = (a0 + span - 1) >> 5;
+                for (int base = wfirst; base <= wlast && found < 0; base += 32) {
+                    const int wi = base + lane;
+                    uint32_t bits = 0;
+                    if (wi <= wlast) {
+                        bits = bm[wi];
+                        if (wi == wfirst) bits &= 0xffffffffu << (a0 & 31);
+                        if (wi == wlast) {
+                            const int e = (a0 + span - 1) & 31;
+                            bits &= (e == 31) ? 0xffffffffu : ((1u << (e + 1)) - 1u);
+                        }
+                    }
+                    const uint32_t ball = __ballot_sync(0xffffffffu, bits != 0);
+                    if (ball) {
+                        const int src = __ffs(ball) - 1;
+                        const uint32_t b = __shfl_sync(0xffffffffu, bits, src);
+                        found = (base + src) * 32 + __ffs(b) - 1;
+                    }
+                }
+            }
+            if (found >= 0) {
+                const int consumed = found - a0 + 1;
+                w.c_mpp += consumed;
+                w.c_coords += 2ull * consumed;
+                w.attempts += consumed;
+                if (lane == 0) {
+                    const int4 cd = ws.cands[(size_t)w.cur_slide * window + found];
+                    emit_spec(cfg, slides[w.cur_slide], descs[w.cur_slide], w.cur_slide, cd.x, cd.y, cd.z,
+                              w.seq, out + w.emitted);
+                }
+                w.seq += 1;
+                w.emitted += 1;
+                w.failures = 0;
+                w.cur_slide = -1;
+            } else if (span == budget) {
+                // exhausted this slide draw (ExhaustedAttemptsError)
+                w.c_mpp += span;
+                w.c_coords += 2ull * span;
+                w.attempts += span;
+                w.cur_slide = -1;
+                w.failures += 1;
+                if (w.failures >= flimit) w.status = PF_ERR_NO_SAMPLABLE;
+            } else {
+                // window (or a rejected draw) reached: consume what was seen
+                w.c_mpp += span;
+                w.c_coords += 2ull * span;
+                w.attempts += span;
+                w.cur_used += span;
+                break;
+            }
+        }
+    }
+    if (finish) {
+        uint32_t* sm = s_masks;
+        while (w.emitted < n && w.status == PF_OK) {
+            if (w.cur_slide < 0) {
+                w.cur_slide = draw_slide(cfg, slides, w.c_slide);
+                w.cur_used = 0;
+            }
+            if (w.cur_used >= max_att) {
+                w.cur_slide = -1;
+                w.failures += 1;
+                if (w.failures >= flimit) w.status = PF_ERR_NO_SAMPLABLE;
+                continue;
+            }
+            slow_attempt(cfg, slides, descs, w, out, sm);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) store_ws(state, w);
+}
+
+__global__ void sample_begin_kernel(pf_sampler_state* state) {
+    state->emitted = 0;
+    state->status = PF_OK;
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" int pf_overlap_fraction(const void* poly_blob_dev, const double* rects_dev, int32_t n,
+                                   int32_t grid, double* out_dev, void* stream) {
+    if (n < 0 || grid < 32 || grid > kMaxGrid || (n > 0 && (!poly_blob_dev || !rects_dev || !out_dev)))
+        return fail(PF_ERR_INVALID_ARG, "pf_overlap_fraction: bad arguments (32 <= grid <= 256)");
+    if (n == 0) return PF_OK;
+    const int warps = 4;
+    const size_t smem = (size_t)warps * overlap_smem_bytes(grid);
+    int rc = check_cuda(cudaFuncSetAttribute(overlap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "cudaFuncSetAttribute");
+    if (rc) return rc;
+    overlap_kernel<<<(n + warps - 1) / warps, warps * 32, smem, as_stream(stream)>>>(poly_blob_dev, rects_dev, n,
+                                                                                 grid, out_dev);
+    return after_launch("overlap_kernel");
+}
+
+extern "C" int pf_sample_workspace_bytes(const pf_sampler_config* cfg, int32_t window, int64_t* bytes) {
+    if (!cfg || !bytes || window < 32 || window % 32 != 0)
+        return fail(PF_ERR_INVALID_ARG, "pf_sample_workspace_bytes: window must be a positive multiple of 32");
+    *bytes = ws_bytes(cfg->n_slides, window);
+    return PF_OK;
+}
+
+extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* slides_dev,
+                         const pf_slide_desc* slide_descs_dev, pf_sampler_state* state_dev, int32_t n,
+                         pf_patch_spec* out_dev, void* workspace, int64_t workspace_bytes, int32_t window,
+                         int32_t rounds, int32_t all_fit, void* stream) {
+    if (!cfg || !slides_dev || !slide_descs_dev || !state_dev || n < 0 || (n > 0 && !out_dev))
+        return fail(PF_ERR_INVALID_ARG, "pf_sample: bad arguments");
+    if (cfg->n_slides < 1) return fail(PF_ERR_NO_SAMPLABLE, "no slides provided");
+    if (cfg->n_mpps < 1 || cfg->n_mpps > PF_MAX_MPPS || cfg->grid < 32 || cfg->grid > kMaxGrid ||
+        cfg->max_attempts < 1)
+        return fail(PF_ERR_INVALID_ARG, "pf_sample: bad config");
+    if (n == 0) return PF_OK;
+    if (window < 32 || window % 32 != 0) rounds = 0;
+    if (rounds > 0 && (!workspace || workspace_bytes < ws_bytes(cfg->n_slides, window)))
+        return fail(PF_ERR_INVALID_ARG, "pf_sample: workspace too small");
+    if (!all_fit) rounds = 0;
+    cudaStream_t st = as_stream(stream);
+    sample_begin_kernel<<<1, 1, 0, st>>>(state_dev);
+    int rc = after_launch("sample_begin_kernel");
+    if (rc) return rc;
+    const int warps = 8;
+    const size_t eval_smem = (size_t)warps * overlap_smem_bytes(cfg->grid);
+    const size_t walk_smem = overlap_smem_bytes(cfg->grid);
+    rc = check_cuda(cudaFuncSetAttribute(sample_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)eval_smem), "cudaFuncSetAttribute");
+    if (rc) return rc;
+    SamplerWs ws{};
+    if (rounds > 0) ws = carve_ws(workspace, cfg->n_slides, window);
+    for (int r = 0; r < rounds; ++r) {
+        const size_t bm_bytes = (size_t)cfg->n_slides * (window / 32) * 4;
+        rc = check_cuda(cudaMemsetAsync(ws.bitmaps, 0, bm_bytes, st), "cudaMemsetAsync");
+        if (rc) return rc;
+        rc = check_cuda(cudaMemsetAsync(ws.reject_at, 0x7f, 4, st), "cudaMemsetAsync");
+        if (rc) return rc;
+        const int64_t cands = (int64_t)cfg->n_slides * window;
+        const int64_t blocks = (cands + warps - 1) / warps;
+        sample_eval_kernel<<<(unsigned)blocks, warps * 32, eval_smem, st>>>(*cfg, slides_dev, state_dev, ws, window, n);
+        if ((rc = after_launch("sample_eval_kernel"))) return rc;
+        sample_walk_kernel<<<1, 32, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws, window, n, 1,
+                                                     r == rounds - 1, out_dev);
+        if ((rc = after_launch("sample_walk_kernel"))) return rc;
+    }
+    if (rounds == 0) {
+        sample_walk_kernel<<<1, 32, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws, window, n, 0, 1,
+                                                     out_dev);
+        if ((rc = after_launch("sample_walk_kernel"))) return rc;
+    }
+    return PF_OK;
+}

@@ -1,0 +1,181 @@
+"""Loader, normalisation and the multi-crop training feed on the GPU.
+
+Mirrors pkg/pipeline.py: ``LoaderConfig`` (43-56), ``run_loader`` (79-149),
+``normalize_patch`` (152-155) and the KPB1 patch pack (158-205).  The thread
+pool of the reference is replaced by batched device reads: ``run_loader``
+keeps its contract (every spec exactly once, ordered by default, skip/raise
+error policy, host (S, S, 3) uint8 arrays out) but assembles up to
+``prefetch_depth`` patches per device call.  ``MultiCropLoader`` is the
+training feed BASELINE config 2 measures: GPU sampler -> fused gather +
+DINOv2 multi-crop -> bf16 NCHW batches that never leave HBM.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import _native as N
+from .errors import LoaderError, PackFormatError
+from .store import GpuSlide, SlideSet, plan_specs
+
+IMAGENET_MEAN = (0.485, 0.456, 0.406)
+IMAGENET_STD = (0.229, 0.224, 0.225)
+
+
+@dataclass
+class LoaderConfig:
+    concurrency: int = 4
+    prefetch_depth: int = 8
+    ordered: bool = True
+    on_error: str = "skip"
+
+    def __post_init__(self):
+        if self.concurrency < 1:
+            raise ValueError("concurrency must be >= 1")
+        if self.prefetch_depth < self.concurrency:
+            raise ValueError("prefetch_depth must be >= concurrency")
+        if self.on_error not in ("skip", "raise"):
+            raise ValueError("on_error must be 'skip' or 'raise'")
+
+
+@dataclass
+class LoaderFailure:
+    spec: object
+    error: Exception
+
+
+class LoaderRun:
+    """Iterator over (spec, pixels); failures collect on ``.errors``."""
+
+    def __init__(self, gen, errors: list):
+        self._gen = gen
+        self.errors = errors
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        return next(self._gen)
+
+
+def run_loader(specs, slides, config: LoaderConfig | None = None, batch: int | None = None) -> LoaderRun:
+    """Load every spec exactly once (pkg/pipeline.py:79-149) with batched GPU reads.
+
+    ``slides``: a GpuSlide or mapping slide_id -> GpuSlide.  Output order is the
+    input order (``ordered`` is honoured trivially); per-spec failures follow
+    ``on_error``.
+    """
+    config = config or LoaderConfig()
+    if isinstance(slides, GpuSlide):
+        slides = {slides.record.slide_id: slides}
+    sset = SlideSet(list(slides.values()))
+    errors: list = []
+    bsz = batch or max(config.prefetch_depth, 64)
+
+    def fail(spec, exc):
+        if config.on_error == "raise":
+            raise LoaderError(f"patch seq {spec.seq} failed: {exc}") from exc
+        errors.append(LoaderFailure(spec, exc))
+
+    def flush(chunk):
+        good, reqs = [], []
+        for sp in chunk:
+            si = sset.index.get(sp.slide_id)
+            if si is None:
+                fail(sp, LoaderError(f"no open slide for id {sp.slide_id!r}"))
+                continue
+            try:
+                plan_specs([(si, sp.rect(), sp.target_mpp, sp.out_size)], sset.records)
+            except Exception as exc:  # noqa: BLE001 - policy decides
+                fail(sp, exc)
+                continue
+            good.append(sp)
+            reqs.append((si, sp.rect(), sp.target_mpp, sp.out_size))
+        # group by out_size (one device call each), then restore input order
+        out = {}
+        for size in sorted({sp.out_size for sp in good}):
+            idx = [i for i, sp in enumerate(good) if sp.out_size == size]
+            arr = plan_specs([reqs[i] for i in idx], sset.records)
+            pix = sset.read_regions(arr, size).cpu().numpy()
+            for j, i in enumerate(idx):
+                out[i] = pix[j]
+        for i, sp in enumerate(good):
+            yield sp, out[i]
+
+    def gen():
+        chunk = []
+        for sp in specs:
+            chunk.append(sp)
+            if len(chunk) >= bsz:
+                yield from flush(chunk)
+                chunk = []
+        if chunk:
+            yield from flush(chunk)
+
+    return LoaderRun(gen(), errors)
+
+
+def normalize_patch(pixels, mean=(0.5, 0.5, 0.5), std=(0.5, 0.5, 0.5), dtype: str = "f32"):
+    """(v/255 - 0.5)/0.5 in FP32 on the GPU (pkg/pipeline.py:152-155); host arrays in -> host out."""
+    torch = N.require_cuda()
+    host = not isinstance(pixels, torch.Tensor)
+    t = torch.from_numpy(np.ascontiguousarray(np.asarray(pixels, dtype=np.uint8))) if host else pixels
+    t = t.to(device="cuda", dtype=torch.uint8).contiguous()
+    if t.shape[-1] != 3:
+        raise ValueError("pixels must be (..., 3) RGB")
+    out = torch.empty(t.shape, dtype=torch.float32 if dtype == "f32" else torch.bfloat16, device="cuda")
+    m = (C.c_float * 3)(*mean)
+    s = (C.c_float * 3)(*std)
+    N.check(N.lib().pf_normalize(t.data_ptr(), t.numel() // 3, N.PF_F32 if dtype == "f32" else N.PF_BF16,
+                                 C.cast(m, C.c_void_p), C.cast(s, C.c_void_p), out.data_ptr(), N.stream_ptr()),
+            "pf_normalize")
+    return out.cpu().numpy() if host else out
+
+
+# ---------------------------------------------------------------------------
+# KPB1 patch pack (pkg/pipeline.py:158-205): format-compatible host I/O.
+PACK_MAGIC = b"KPB1"
+_PACK_HEADER = struct.Struct("<4sIIIB3x")
+_DTYPE_TAGS = {np.dtype(np.uint8): 0, np.dtype(np.float32): 1}
+_TAG_DTYPES = {0: np.dtype(np.uint8), 1: np.dtype(np.float32)}
+
+
+def write_patch_pack(patches, path, specs=None) -> Path:
+    arr = patches.cpu().numpy() if hasattr(patches, "cpu") else np.asarray(patches)
+    if arr.ndim != 4 or arr.shape[3] != 3 or arr.shape[1] != arr.shape[2]:
+        raise PackFormatError(f"patches must be (count, size, size, 3), got {arr.shape}")
+    tag = _DTYPE_TAGS.get(arr.dtype)
+    if tag is None:
+        raise PackFormatError(f"unsupported dtype {arr.dtype}; use uint8 or float32")
+    path = Path(path)
+    with open(path, "wb") as fh:
+        fh.write(_PACK_HEADER.pack(PACK_MAGIC, arr.shape[0], arr.shape[1], 3, tag))
+        fh.write(np.ascontiguousarray(arr).astype(arr.dtype.newbyteorder("<")).tobytes())
+    if specs is not None:
+        with open(path.with_name(path.name + ".manifest.jsonl"), "w", encoding="utf-8") as fh:
+            for sp in specs:
+                fh.write(sp.to_json_line() + "\n")
+    return path
+
+
+def read_patch_pack(path) -> np.ndarray:
+    data = Path(path).read_bytes()
+    if len(data) < _PACK_HEADER.size:
+        raise PackFormatError("file too short for a pack header")
+    magic, count, size, ch, tag = _PACK_HEADER.unpack_from(data)
+    if magic != PACK_MAGIC:
+        raise PackFormatError(f"bad magic {magic!r}")
+    if ch != 3:
+        raise PackFormatError(f"channels must be 3, header says {ch}")
+    dt = _TAG_DTYPES.get(tag)
+    if dt is None:
+        raise PackFormatError(f"unknown dtype tag {tag}")
+    payload = data[_PACK_HEADER.size:]
+    if len(payload) != count * size * size * 3 * dt.itemsize:
+        raise PackFormatError(f"payload is {len(payload)} bytes, header implies {count * size * size * 3 * dt.itemsize}")
+    return np.frombuffer(payload, dtype=dt.newbyteorder("<")).reshape(count, size, size, 3).astype(dt)

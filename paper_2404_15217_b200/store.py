@@ -1,0 +1,430 @@
+"""HBM-resident slide pyramids and the batched region reader.
+
+Mirrors the read side of pkg/store.py: ``SlideRecord``/``LevelInfo``
+(115-237), ``select_level`` (568-581), ``round_half_away`` (70-72),
+``Slide.thumbnail`` (604-609) and ``Slide.read_region`` (651-688).  Instead of
+a host tile cache fed by a transport, every level lives in HBM in the padded
+tile-major layout of include/pf_b200.h, built on the GPU by the reference's
+box filter (``_box_downsample``, 429-441) with the ingest stopping rule
+(496-498).  ``GpuSlide`` duck-types the reference ``Slide`` (``.record`` +
+``.read_region``) so it plugs into ``run_loader``; ``read_regions`` is the
+batched device path.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from . import _native as N
+from .errors import DecodeError, IntegrityError, OutOfBoundsError, SlideNotFoundError, StoreError
+
+STORE_FORMAT_VERSION = 1
+
+
+def round_half_away(x: float) -> int:
+    """Round half away from zero (pkg/store.py:70-72)."""
+    return int(math.floor(x + 0.5)) if x >= 0 else int(math.ceil(x - 0.5))
+
+
+@dataclass(frozen=True)
+class LevelInfo:
+    width: int
+    height: int
+    mpp: float
+    downsample: int
+
+
+@dataclass
+class SlideRecord:
+    """Pyramid metadata (pkg/store.py:122-237); ``chunks`` only for store-backed slides."""
+
+    slide_id: str
+    base_mpp: float
+    tile_size: int
+    levels: list
+    chunks: dict = field(default_factory=dict)
+
+    @property
+    def width(self) -> int:
+        return self.levels[0].width
+
+    @property
+    def height(self) -> int:
+        return self.levels[0].height
+
+    def tile_grid(self, level: int) -> tuple:
+        lv = self.levels[level]
+        t = self.tile_size
+        return -(-lv.width // t), -(-lv.height // t)
+
+    def tile_dims(self, level: int, tx: int, ty: int) -> tuple:
+        lv = self.levels[level]
+        t = self.tile_size
+        return min(t, lv.width - tx * t), min(t, lv.height - ty * t)
+
+    def validate(self) -> None:
+        """Level invariants of SlideRecord.validate (pkg/store.py:151-176)."""
+        if self.tile_size < 16:
+            raise IntegrityError(f"tile_size {self.tile_size} < 16")
+        if not self.levels:
+            raise IntegrityError("record has no levels")
+        l0 = self.levels[0]
+        if l0.downsample != 1:
+            raise IntegrityError("level 0 must have downsample 1")
+        if not math.isclose(l0.mpp, self.base_mpp, rel_tol=1e-9):
+            raise IntegrityError("level 0 mpp must equal base_mpp")
+        prev = 0.0
+        for i, lv in enumerate(self.levels):
+            if lv.mpp <= prev:
+                raise IntegrityError(f"levels not sorted by increasing mpp at {i}")
+            prev = lv.mpp
+            if not math.isclose(lv.mpp, self.base_mpp * lv.downsample, rel_tol=1e-9):
+                raise IntegrityError(f"level {i} mpp {lv.mpp} != base_mpp * downsample")
+            ew, eh = -(-l0.width // lv.downsample), -(-l0.height // lv.downsample)
+            if abs(lv.width - ew) > 1 or abs(lv.height - eh) > 1:
+                raise IntegrityError(
+                    f"level {i} dims ({lv.width}x{lv.height}) do not match level 0 / downsample ({ew}x{eh})"
+                )
+
+    def to_json_dict(self) -> dict:
+        return {
+            "slide_id": self.slide_id,
+            "base_mpp": self.base_mpp,
+            "tile_size": self.tile_size,
+            "levels": [
+                {"width_px": lv.width, "height_px": lv.height, "mpp": lv.mpp, "downsample": lv.downsample}
+                for lv in self.levels
+            ],
+            "chunks": {f"{k[0]}/{k[1]}_{k[2]}": v for k, v in sorted(self.chunks.items())},
+        }
+
+    @classmethod
+    def from_json_dict(cls, doc: dict) -> "SlideRecord":
+        try:
+            levels = [
+                LevelInfo(int(d["width_px"]), int(d["height_px"]), float(d["mpp"]), int(d["downsample"]))
+                for d in doc["levels"]
+            ]
+            chunks = {}
+            for key, loc in doc.get("chunks", {}).items():
+                li, rest = key.split("/")
+                tx, ty = rest.split("_")
+                chunks[(int(li), int(tx), int(ty))] = dict(loc)
+            return cls(str(doc["slide_id"]), float(doc["base_mpp"]), int(doc["tile_size"]), levels, chunks)
+        except (KeyError, ValueError) as exc:
+            raise IntegrityError(f"malformed slide record: {exc}") from exc
+
+
+def select_level(record: SlideRecord, target_mpp: float) -> int:
+    """argmin |ln(mpp_i / target)|, ties (within 1e-12) to the finer level (pkg/store.py:568-581)."""
+    if target_mpp <= 0:
+        raise ValueError("target_mpp must be positive")
+    best, best_d = 0, math.inf
+    for i, lv in enumerate(record.levels):
+        d = abs(math.log(lv.mpp / target_mpp))
+        if d < best_d - 1e-12:
+            best, best_d = i, d
+    return best
+
+
+def pyramid_dims(width: int, height: int, tile_size: int, factor: int) -> list:
+    """Level dims of ingest_image: repeat ceil-divide by `factor` until max(dim) <= tile (store.py:496-498)."""
+    dims = [(width, height)]
+    while max(dims[-1]) > tile_size:
+        w, h = dims[-1]
+        dims.append((-(-w // factor), -(-h // factor)))
+    return dims
+
+
+def make_record(slide_id: str, width: int, height: int, base_mpp: float, tile_size: int = 256,
+                downsample_factor: int = 2) -> SlideRecord:
+    dims = pyramid_dims(width, height, tile_size, downsample_factor)
+    levels = [
+        LevelInfo(w, h, base_mpp * downsample_factor**i, downsample_factor**i) for i, (w, h) in enumerate(dims)
+    ]
+    rec = SlideRecord(slide_id, base_mpp, tile_size, levels)
+    rec.validate()
+    return rec
+
+
+def _tiles_from_hwc(arr: np.ndarray, tile: int) -> np.ndarray:
+    """(H, W, 3) -> padded tile-major (ty, tx, T, T, 3)."""
+    h, w = arr.shape[:2]
+    ny, nx = -(-h // tile), -(-w // tile)
+    pad = np.zeros((ny * tile, nx * tile, 3), dtype=np.uint8)
+    pad[:h, :w] = arr
+    return np.ascontiguousarray(pad.reshape(ny, tile, nx, tile, 3).transpose(0, 2, 1, 3, 4))
+
+
+class GpuSlide:
+    """A slide pyramid resident in HBM (drop-in for the reference ``Slide``)."""
+
+    def __init__(self, record: SlideRecord, levels, factor: int):
+        self.record = record
+        self.levels = levels  # torch uint8 [ty, tx, T, T, 3] per level
+        self.factor = factor
+        self.desc = self._make_desc()
+
+    # -- construction -----------------------------------------------------
+    @classmethod
+    def allocate(cls, slide_id: str, width: int, height: int, base_mpp: float, tile_size: int = 256,
+                 downsample_factor: int = 2, device=None) -> "GpuSlide":
+        torch = N.require_cuda()
+        rec = make_record(slide_id, width, height, base_mpp, tile_size, downsample_factor)
+        levels = []
+        for li in range(len(rec.levels)):
+            nx, ny = rec.tile_grid(li)
+            levels.append(torch.empty((ny, nx, tile_size, tile_size, 3), dtype=torch.uint8, device=device or "cuda"))
+        return cls(rec, levels, downsample_factor)
+
+    @classmethod
+    def from_array(cls, pixels, slide_id: str, base_mpp: float, *, tile_size: int = 256,
+                   downsample_factor: int = 2, stream=None) -> "GpuSlide":
+        """ingest_image (pkg/store.py:462-565) into HBM: level 0 uploaded, upper levels box-filtered on device."""
+        torch = N.require_cuda()
+        arr = pixels.cpu().numpy() if hasattr(pixels, "cpu") else np.asarray(pixels)
+        if arr.ndim != 3 or arr.shape[2] != 3 or arr.dtype != np.uint8:
+            raise ValueError("pixels must be an (H, W, 3) uint8 array")
+        if arr.shape[0] < 1 or arr.shape[1] < 1:
+            raise ValueError("image must be at least 1x1")
+        if tile_size < 16:
+            raise ValueError("tile_size must be >= 16")
+        if downsample_factor < 2:
+            raise ValueError("downsample_factor must be >= 2")
+        slide = cls.allocate(slide_id, arr.shape[1], arr.shape[0], base_mpp, tile_size, downsample_factor)
+        slide.levels[0].copy_(torch.from_numpy(_tiles_from_hwc(arr, tile_size)))
+        slide.build_pyramid(stream)
+        return slide
+
+    @classmethod
+    def from_store(cls, store_root, slide_id: str, stream=None) -> "GpuSlide":
+        """Load a reference store slide (index.json + slides/<id>.json + chunks) into HBM.
+
+        Every level is read as stored (raw/png/jpeg via the store's locators) so the
+        HBM pyramid holds the exact bytes the reference serves.
+        """
+        torch = N.require_cuda()
+        root = Path(store_root)
+        idx_path = root / "index.json"
+        if not idx_path.exists():
+            raise StoreError(f"no store at {store_root} (missing index.json)")
+        index = json.loads(idx_path.read_text(encoding="utf-8"))
+        if int(index.get("format_version", -1)) != STORE_FORMAT_VERSION:
+            raise IntegrityError(f"unsupported store format_version {index.get('format_version')}")
+        if slide_id not in index.get("slides", []):
+            raise SlideNotFoundError(f"slide {slide_id!r} not in store {root}")
+        rel = index.get("records", {}).get(slide_id, f"slides/{slide_id}.json")
+        rec = SlideRecord.from_json_dict(json.loads((root / rel).read_text(encoding="utf-8")))
+        if rec.slide_id != slide_id:
+            raise IntegrityError(f"record names slide {rec.slide_id!r}, expected {slide_id!r}")
+        rec.validate()
+        factor = rec.levels[1].downsample if len(rec.levels) > 1 else 2
+        T = rec.tile_size
+        levels = []
+        for li, lv in enumerate(rec.levels):
+            nx, ny = rec.tile_grid(li)
+            host = np.zeros((ny, nx, T, T, 3), dtype=np.uint8)
+            for ty in range(ny):
+                for tx in range(nx):
+                    loc = rec.chunks.get((li, tx, ty))
+                    if loc is None:
+                        raise IntegrityError(f"missing chunk locator ({li}, {tx}, {ty})")
+                    tw, th = rec.tile_dims(li, tx, ty)
+                    host[ty, tx, :th, :tw] = _read_chunk(root, loc, tw, th)
+            levels.append(torch.from_numpy(host).cuda())
+        return cls(rec, levels, factor)
+
+    def build_pyramid(self, stream=None) -> None:
+        """Levels 1.. from level 0 with the reference box filter, on device."""
+        for li in range(1, len(self.record.levels)):
+            N.check(N.lib().pf_build_level(self.desc, li, self.factor, N.stream_ptr(stream)), "pf_build_level")
+
+    def _make_desc(self) -> N.SlideDesc:
+        d = N.SlideDesc()
+        rec = self.record
+        if len(rec.levels) > N.PF_MAX_LEVELS:
+            raise ValueError(f"more than {N.PF_MAX_LEVELS} pyramid levels")
+        for i, lv in enumerate(rec.levels):
+            nx, ny = rec.tile_grid(i)
+            d.level_ptr[i] = int(self.levels[i].data_ptr()) if self.levels else 0
+            d.mpp[i] = lv.mpp
+            d.width[i] = lv.width
+            d.height[i] = lv.height
+            d.tiles_x[i] = nx
+            d.tiles_y[i] = ny
+            d.downsample[i] = lv.downsample
+        d.n_levels = len(rec.levels)
+        d.tile_size = rec.tile_size
+        d.base_mpp = rec.base_mpp
+        return d
+
+    # -- reads ------------------------------------------------------------
+    def select_level(self, target_mpp: float) -> int:
+        return select_level(self.record, target_mpp)
+
+    def level_array(self, li: int):
+        """Level li as a dense (H, W, 3) uint8 device tensor (copy)."""
+        lv = self.record.levels[li]
+        t = self.levels[li]
+        ny, nx, T = t.shape[0], t.shape[1], t.shape[2]
+        return t.permute(0, 2, 1, 3, 4).reshape(ny * T, nx * T, 3)[: lv.height, : lv.width].contiguous()
+
+    def thumbnail_device(self, factor: int | None = None, src_level: int = 0, stream=None):
+        """(device (h, w, 3) uint8, scale).  factor None -> coarsest level (Slide.thumbnail)."""
+        torch = N.require_cuda()
+        if factor is None:
+            src_level, factor = len(self.record.levels) - 1, 1
+        lv = self.record.levels[src_level]
+        out = torch.empty((-(-lv.height // factor), -(-lv.width // factor), 3), dtype=torch.uint8, device="cuda")
+        N.check(N.lib().pf_thumbnail(self.desc, src_level, factor, out.data_ptr(), N.stream_ptr(stream)), "pf_thumbnail")
+        return out, 1.0 / (lv.downsample * factor)
+
+    def thumbnail(self, factor: int | None = None) -> tuple:
+        """Drop-in Slide.thumbnail (pkg/store.py:604-609): (host ndarray, scale)."""
+        t, scale = self.thumbnail_device(factor)
+        return t.cpu().numpy(), scale
+
+    def read_region(self, rect_level0, target_mpp: float, out_size: int) -> np.ndarray:
+        """Drop-in Slide.read_region (pkg/store.py:651-688): (out, out, 3) uint8 host array."""
+        specs = plan_specs([(0, rect_level0, target_mpp, out_size)], [self.record])
+        if getattr(self, "_own_set", None) is None:
+            self._own_set = SlideSet([self])
+        out = self._own_set.read_regions(specs, out_size)
+        return out[0].cpu().numpy()
+
+
+def _read_chunk(root: Path, loc: dict, tw: int, th: int) -> np.ndarray:
+    path = loc["path"]
+    p = Path(path) if Path(path).is_absolute() else root / path
+    try:
+        if loc["kind"] == "byte-range":
+            with open(p, "rb") as fh:
+                fh.seek(int(loc["offset"]))
+                data = fh.read(int(loc["length"]))
+        else:
+            data = p.read_bytes()
+    except OSError as exc:
+        raise StoreError(f"cannot read {p}: {exc}") from exc
+    if loc["codec"] == "raw":
+        if len(data) != tw * th * 3:
+            raise DecodeError(f"raw tile has {len(data)} bytes, expected {tw * th * 3}")
+        return np.frombuffer(data, dtype=np.uint8).reshape(th, tw, 3)
+    import io
+
+    from PIL import Image
+
+    try:
+        arr = np.asarray(Image.open(io.BytesIO(data)).convert("RGB"))
+    except Exception as exc:  # noqa: BLE001 - mirrors decode_tile's catch-all
+        raise DecodeError(f"cannot decode {loc['codec']} tile: {exc}") from exc
+    if arr.shape[:2] != (th, tw):
+        raise DecodeError(f"decoded tile is {arr.shape[1]}x{arr.shape[0]}, expected {tw}x{th}")
+    return arr
+
+
+def plan_specs(requests, records) -> np.ndarray:
+    """Host read plan for explicit region requests.
+
+    requests: iterable of (slide_index, (x, y, w, h), target_mpp, out_size).
+    Validates bounds exactly like read_region/_read_window (pkg/store.py:667-702)
+    and fills level/side; sx/sy are filled on device (pf_plan_regions).
+    """
+    reqs = list(requests)
+    specs = np.zeros(len(reqs), dtype=N.SPEC_DTYPE)
+    level_cache: dict = {}
+    for i, (si, rect, mpp, out_size) in enumerate(reqs):
+        rec = records[si]
+        x, y, w, h = (int(v) for v in rect)
+        if out_size < 1:
+            raise ValueError("out_size must be >= 1")
+        if w < 1 or h < 1:
+            raise OutOfBoundsError("rect must have positive extent")
+        if x < 0 or y < 0 or x + w > rec.width or y + h > rec.height:
+            raise OutOfBoundsError(f"rect {tuple(rect)} outside level-0 bounds {rec.width}x{rec.height}")
+        key = (si, float(mpp))
+        if key not in level_cache:
+            level_cache[key] = select_level(rec, float(mpp))
+        li = level_cache[key]
+        lv = rec.levels[li]
+        side = max(1, round_half_away(out_size * mpp / lv.mpp))
+        sx, sy = round_half_away(x / lv.downsample), round_half_away(y / lv.downsample)
+        if sx < -1 or sy < -1 or sx + side > lv.width + 1 or sy + side > lv.height + 1:
+            raise OutOfBoundsError(f"window ({sx}, {sy}, {side}, {side}) outside level {li} ({lv.width}x{lv.height})")
+        if side != out_size and 2 * math.ceil(max(side / out_size, 1.0)) + 1 > 32:
+            raise ValueError(f"down-ratio {side}/{out_size} too large for the resampler")
+        specs[i] = (i, mpp, si, x, y, w, h, out_size, -1, li, side, sx, sy, 0)
+    return specs
+
+
+class SlideSet:
+    """Slides addressed by index in one device call (pf_slide_desc array in HBM)."""
+
+    def __init__(self, slides):
+        torch = N.require_cuda()
+        self.slides = list(slides)
+        self.ids = [s.record.slide_id for s in self.slides]
+        if len(set(self.ids)) != len(self.ids):
+            raise ValueError("duplicate slide ids")
+        self.index = {sid: i for i, sid in enumerate(self.ids)}
+        raw = b"".join(bytes(s.desc) for s in self.slides)
+        self.descs = torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
+
+    def __len__(self):
+        return len(self.slides)
+
+    @property
+    def records(self):
+        return [s.record for s in self.slides]
+
+    def specs_to_device(self, specs):
+        import torch
+
+        if isinstance(specs, torch.Tensor):
+            return specs
+        arr = np.ascontiguousarray(specs, dtype=N.SPEC_DTYPE)
+        return torch.from_numpy(arr.view(np.uint8).reshape(len(arr), 64)).cuda(non_blocking=False)
+
+    def read_regions(self, specs, out_size: int, *, dtype: str = "u8", layout: str = "hwc", mean=(0.5, 0.5, 0.5),
+                     std=(0.5, 0.5, 0.5), out=None, stream=None, planned: bool = False):
+        """Batched read_region on device -> tensor [n, S, S, 3] (hwc) or [n, 3, S, S] (nchw).
+
+        dtype "u8" returns raw pixels; "f32"/"bf16" apply (v/255 - mean)/std
+        (normalize_patch, pkg/pipeline.py:152-155, for mean = std = 0.5).
+        """
+        torch = N.require_cuda()
+        dspecs = self.specs_to_device(specs)
+        n = dspecs.shape[0]
+        dt = {"u8": (N.PF_U8, torch.uint8), "f32": (N.PF_F32, torch.float32), "bf16": (N.PF_BF16, torch.bfloat16)}
+        code, tdt = dt[dtype]
+        lay = {"hwc": N.PF_HWC, "nchw": N.PF_NCHW}[layout]
+        shape = (n, out_size, out_size, 3) if lay == N.PF_HWC else (n, 3, out_size, out_size)
+        if out is None:
+            out = torch.empty(shape, dtype=tdt, device="cuda")
+        sp = N.stream_ptr(stream)
+        if not planned:
+            N.check(N.lib().pf_plan_regions(self.descs.data_ptr(), dspecs.data_ptr(), n, sp), "pf_plan_regions")
+        m = (N.C.c_float * 3)(*mean)
+        s = (N.C.c_float * 3)(*std)
+        N.check(
+            N.lib().pf_read_regions(self.descs.data_ptr(), dspecs.data_ptr(), n, out_size, code, lay,
+                                    N.C.cast(m, N.C.c_void_p), N.C.cast(s, N.C.c_void_p), out.data_ptr(), sp),
+            "pf_read_regions",
+        )
+        return out
+
+    def read_specs(self, patch_specs, *, dtype="u8", layout="hwc", mean=(0.5, 0.5, 0.5), std=(0.5, 0.5, 0.5)):
+        """read_regions for reference PatchSpec objects (uniform out_size)."""
+        ps = list(patch_specs)
+        if not ps:
+            raise ValueError("no specs")
+        sizes = {p.out_size for p in ps}
+        if len(sizes) != 1:
+            raise ValueError("read_specs needs a uniform out_size")
+        specs = plan_specs([(self.index[p.slide_id], p.rect(), p.target_mpp, p.out_size) for p in ps], self.records)
+        specs["seq"] = [p.seq for p in ps]
+        return self.read_regions(specs, ps[0].out_size, dtype=dtype, layout=layout, mean=mean, std=std)

@@ -1,0 +1,135 @@
+"""GPU parity: pyramid build, thumbnails, read_region (gather + PIL resample) and normalisation
+against the oracle and the reference goldens.  Bit-exact (integer / byte work)."""
+
+import numpy as np
+import pytest
+
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pf(cuda):
+    import paper_2404_15217_b200 as pf
+
+    return pf
+
+
+def test_pyramid_and_thumbnail_match_reference(pf, goldens, golden_arrays):
+    img = golden_arrays["synthetic_700x500"]
+    s = pf.GpuSlide.from_array(img, "s0", 0.25, tile_size=128, downsample_factor=2)
+    assert [(lv.width, lv.height, lv.mpp, lv.downsample) for lv in s.record.levels] == [tuple(x) for x in goldens["levels_f2_t128"]]
+    for li in range(len(s.record.levels)):
+        assert np.array_equal(s.level_array(li).cpu().numpy(), golden_arrays[f"level_f2_{li}"]), li
+    th, sc = s.thumbnail()
+    assert np.array_equal(th, golden_arrays["thumb_f2"]) and sc == goldens["thumb_f2_scale"]
+    t32, sc32 = s.thumbnail(32)
+    assert np.array_equal(t32, golden_arrays["box32_700x500"]) and sc32 == 1 / 32
+    t7, _ = s.thumbnail(7)
+    assert np.array_equal(t7, golden_arrays["box7_700x500"])
+    s4 = pf.GpuSlide.from_array(img, "s1", 0.25, tile_size=64, downsample_factor=4)
+    assert np.array_equal(s4.level_array(1).cpu().numpy(), golden_arrays["level_f4_1"])
+
+
+def test_box32_fast_path_large(pf):
+    rs = np.random.default_rng(0)
+    img = rs.integers(0, 256, size=(1000, 1333, 3), dtype=np.uint8)
+    s = pf.GpuSlide.from_array(img, "big", 0.25, tile_size=256, downsample_factor=4)
+    t, _ = s.thumbnail(32)
+    assert np.array_equal(t, port.box_downsample(img, 32))
+    for li, want in enumerate(port.pyramid(img, 256, 4)):
+        assert np.array_equal(s.level_array(li).cpu().numpy(), want)
+
+
+def test_read_region_matches_reference(pf, goldens, golden_arrays):
+    img = golden_arrays["synthetic_700x500"]
+    s = pf.GpuSlide.from_array(img, "s0", 0.25, tile_size=128, downsample_factor=2)
+    for r in goldens["reads"]:
+        got = s.read_region(tuple(r["rect"]), r["mpp"], r["out"])
+        assert np.array_equal(got, golden_arrays[f"read_{r['k']}"]), r
+
+
+def test_read_regions_batched_all_layouts(pf, goldens, golden_arrays, cuda):
+    torch = cuda
+    img = golden_arrays["synthetic_700x500"]
+    s = pf.GpuSlide.from_array(img, "s0", 0.25, tile_size=128, downsample_factor=2)
+    ss = pf.SlideSet([s])
+    reads = [r for r in goldens["reads"] if r["out"] == 32]
+    specs = pf.store.plan_specs([(0, r["rect"], r["mpp"], 32) for r in reads], ss.records)
+    want = np.stack([golden_arrays[f"read_{r['k']}"] for r in reads])
+    hwc = ss.read_regions(specs, 32).cpu().numpy()
+    assert np.array_equal(hwc, want)
+    nchw = ss.read_regions(specs, 32, layout="nchw").cpu().numpy()
+    assert np.array_equal(nchw, want.transpose(0, 3, 1, 2))
+    f32 = ss.read_regions(specs, 32, dtype="f32", layout="nchw").cpu().numpy()
+    assert np.array_equal(f32, port.normalize_patch(want).transpose(0, 3, 1, 2))  # bit-exact FP32
+    mean, std = pf.IMAGENET_MEAN, pf.IMAGENET_STD
+    f32i = ss.read_regions(specs, 32, dtype="f32", layout="nchw", mean=mean, std=std).cpu().numpy()
+    assert np.array_equal(f32i, port.normalize_patch(want, mean, std).transpose(0, 3, 1, 2))
+    b16 = ss.read_regions(specs, 32, dtype="bf16", layout="nchw", mean=mean, std=std)
+    ref16 = torch.from_numpy(port.normalize_patch(want, mean, std).transpose(0, 3, 1, 2).copy()).to(torch.bfloat16)
+    assert torch.equal(b16.cpu(), ref16)
+
+
+def test_edge_replication_and_bounds(pf):
+    rs = np.random.default_rng(3)
+    img = rs.integers(0, 256, size=(301, 257, 3), dtype=np.uint8)
+    s = pf.GpuSlide.from_array(img, "e", 0.25, tile_size=64, downsample_factor=2)
+    lv = port.pyramid(img, 64, 2)
+    mpps = [lv_.mpp for lv_ in s.record.levels]
+    ds = [lv_.downsample for lv_ in s.record.levels]
+    # windows at the far edges at coarse levels overrun by the 1-px slack
+    for rect, mpp, out in [((256, 300, 1, 1), 0.5, 3), ((250, 290, 7, 11), 1.0, 5), ((0, 0, 257, 301), 2.0, 32),
+                           ((255, 299, 2, 2), 4.0, 2), ((254, 298, 3, 3), 0.5, 3), ((252, 296, 5, 5), 2.0, 1), ((3, 5, 200, 200), 0.25, 200), ((0, 0, 4, 4), 8.0, 9)]:
+        try:
+            want = port.read_region(lv, mpps, ds, rect, mpp, out)
+        except IndexError:  # the reference's _read_window slack rule rejects it too
+            with pytest.raises(pf.OutOfBoundsError):
+                s.read_region(rect, mpp, out)
+            continue
+        assert np.array_equal(s.read_region(rect, mpp, out), want), (rect, mpp, out)
+    with pytest.raises(pf.OutOfBoundsError):
+        s.read_region((250, 0, 10, 10), 0.25, 10)
+    with pytest.raises(pf.OutOfBoundsError):
+        s.read_region((0, 0, 0, 10), 0.25, 10)
+    with pytest.raises(ValueError):
+        s.read_region((0, 0, 10, 10), 0.25, 0)
+
+
+def test_normalize_patch_kats(pf, goldens):
+    v = pf.normalize_patch(np.array([[0, 255, 128], [1, 254, 7]], np.uint8).reshape(1, 2, 3))
+    assert v.reshape(-1)[:3].tolist() == goldens["normalize"][:3]
+    assert v.reshape(-1)[3:5].tolist() == goldens["normalize"][3:5]
+
+
+def test_store_roundtrip_from_reference_format(pf, tmp_path, golden_arrays):
+    """A store written in the reference on-disk format (raw, packed) loads into HBM byte-exactly."""
+    import json
+
+    img = golden_arrays["synthetic_700x500"]
+    levels = port.pyramid(img, 128, 4)
+    root = tmp_path / "store"
+    (root / "chunks").mkdir(parents=True)
+    (root / "slides").mkdir()
+    chunks, off, blob = {}, 0, bytearray()
+    for li, a in enumerate(levels):
+        ny, nx = -(-a.shape[0] // 128), -(-a.shape[1] // 128)
+        for ty in range(ny):
+            for tx in range(nx):
+                t = np.ascontiguousarray(a[ty * 128:(ty + 1) * 128, tx * 128:(tx + 1) * 128]).tobytes()
+                chunks[f"{li}/{tx}_{ty}"] = {"kind": "byte-range", "path": "chunks/s.bin", "codec": "raw", "offset": off,
+                                             "length": len(t)}
+                blob += t
+                off += len(t)
+    (root / "chunks" / "s.bin").write_bytes(bytes(blob))
+    rec = {"slide_id": "s", "base_mpp": 0.25, "tile_size": 128, "chunks": chunks,
+           "levels": [{"width_px": a.shape[1], "height_px": a.shape[0], "mpp": 0.25 * 4**i, "downsample": 4**i}
+                      for i, a in enumerate(levels)]}
+    (root / "slides" / "s.json").write_text(json.dumps(rec))
+    (root / "index.json").write_text(json.dumps({"format_version": 1, "slides": ["s"], "records": {"s": "slides/s.json"}}))
+    s = pf.GpuSlide.from_store(root, "s")
+    for li, a in enumerate(levels):
+        assert np.array_equal(s.level_array(li).cpu().numpy(), a)
+    with pytest.raises(pf.SlideNotFoundError):
+        pf.GpuSlide.from_store(root, "nope")
