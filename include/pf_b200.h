@@ -45,8 +45,11 @@ enum pf_status {
 /* Output element types for the normalising epilogues. */
 enum pf_dtype { PF_U8 = 0, PF_F32 = 1, PF_BF16 = 2 };
 
-/* Output layouts for pf_read_regions. */
+/* Output layouts for pf_read_regions.  OR with PF_SKIP_PASSTHROUGH to leave
+ * the output of specs with side == out_size untouched (the multi-crop kernel
+ * reads those straight from the pyramid). */
 enum pf_layout { PF_HWC = 0, PF_NCHW = 1 };
+#define PF_SKIP_PASSTHROUGH 256
 
 /* Tissue-mask rules for pf_mask. */
 enum pf_mask_mode {
@@ -279,6 +282,9 @@ typedef struct pf_crop_param {
  * n_patches * (n_global + n_local) records, patch-major. */
 int pf_crop_params(uint64_t seed, int32_t rank, uint64_t step, int32_t n_patches,
                    const pf_multicrop_config* cfg, pf_crop_param* out_dev, void* stream);
+
+/* One Philox4x32-10 block (Random123 semantics): out = philox(ctr, key). */
+void pf_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 
 /* Fused gather + RandomResizedCrop (torch uint8 antialiased bilinear) + flip
  * + ColorJitter (per-op uint8 quantisation, per-crop order) + grayscale +

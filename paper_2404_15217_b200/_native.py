@@ -33,6 +33,7 @@ PF_ERR_INTERNAL = 9
 
 PF_U8, PF_F32, PF_BF16 = 0, 1, 2
 PF_HWC, PF_NCHW = 0, 1
+PF_SKIP_PASSTHROUGH = 256
 PF_MASK_LUMINANCE, PF_MASK_SATURATION = 0, 1
 
 PF_AUG_FLIP, PF_AUG_JITTER, PF_AUG_GRAY, PF_AUG_BLUR, PF_AUG_SOLARIZE = 1, 2, 4, 8, 16
@@ -195,6 +196,7 @@ class _Lib:
                 [vp, vp, vp, i32, vp, C.POINTER(MultiCropConfig), i32, vp, vp, vp, vp, vp],
                 C.c_int,
             ),
+            "pf_philox4x32_10": ([vp, vp, vp], None),
             "pf_synth_level0": ([C.POINTER(SlideDesc), vp, i32, i32, i32, C.c_float, u64, vp], C.c_int),
         }
         self.symbols = sorted(sig)

@@ -157,8 +157,11 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
     const int L = sp.level;
     const int W = s.width[L], H = s.height[L];
     const int side = sp.side, S = out_size;
+    const bool skip_pass = layout & PF_SKIP_PASSTHROUGH;
+    layout &= 0xff;
 
     if (side == S) {
+        if (skip_pass) return;
         for (int p = threadIdx.x; p < S * S; p += blockDim.x) {
             const int y = p / S, x = p - y * S;
             const int X = clampi(sp.sx + x, 0, W - 1), Y = clampi(sp.sy + y, 0, H - 1);
@@ -307,7 +310,7 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
                                const float* mean3, const float* std3, void* out, void* stream) {
     if (n < 0 || out_size < 1 || out_size > 4096 || (n > 0 && (!slides_dev || !specs_dev || !out)))
         return fail(PF_ERR_INVALID_ARG, "pf_read_regions: bad arguments");
-    if (layout != PF_HWC && layout != PF_NCHW)
+    if ((layout & 0xff) != PF_HWC && (layout & 0xff) != PF_NCHW)
         return fail(PF_ERR_INVALID_ARG, "pf_read_regions: bad layout");
     if (out_size > 512)
         return fail(PF_ERR_INVALID_ARG, "pf_read_regions: out_size > 512 unsupported");

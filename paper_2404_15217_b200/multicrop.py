@@ -1,0 +1,196 @@
+"""DINOv2 multi-crop training feed on the GPU (BASELINE.json configs 2-5).
+
+The reference stops at ``read_region`` + ``normalize_patch`` (SURVEY.md §0.1
+D5); BASELINE config 2 asks for the DINOv2 multi-crop on every sampled patch:
+2 global 224^2 crops (RandomResizedCrop scale (0.32, 1)) and 8 local 96^2
+crops (scale (0.05, 0.32)), hflip p=0.5, ColorJitter(0.4, 0.4, 0.2, 0.1)
+p=0.8, grayscale p=0.2, gaussian blur sigma U(0.1, 2) with p = 1.0 / 0.1 /
+0.5, solarize p=0.2 on the second global crop, ImageNet normalisation, bf16.
+
+Per-crop parameters come from Philox4x32-10 keyed by (seed, rank) with
+counter (step, patch, crop) (pf_crop_params) and are explicit records, so the
+torchvision oracle can replay them.  ``MultiCropLoader`` chains the device
+sampler, the PIL resample for patches read off-level (mixed mpp, config 3),
+the parameter generator and the fused kernel on one CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .pipeline import IMAGENET_MEAN, IMAGENET_STD
+
+
+@dataclass
+class MultiCropConfig:
+    n_global: int = 2
+    n_local: int = 8
+    global_size: int = 224
+    local_size: int = 96
+    src_size: int = 224
+    global_scale: tuple = (0.32, 1.0)
+    local_scale: tuple = (0.05, 0.32)
+    ratio: tuple = (3.0 / 4.0, 4.0 / 3.0)
+    p_flip: float = 0.5
+    p_jitter: float = 0.8
+    p_gray: float = 0.2
+    brightness: float = 0.4
+    contrast: float = 0.4
+    saturation: float = 0.2
+    hue: float = 0.1
+    sigma: tuple = (0.1, 2.0)
+    p_blur: list = field(default_factory=lambda: [1.0, 0.1] + [0.5] * 8)
+    p_solarize: list = field(default_factory=lambda: [0.0, 0.2] + [0.0] * 8)
+    solarize_threshold: float = 128.0
+    blur_kernel: int = 9
+
+    def __post_init__(self):
+        n = self.n_global + self.n_local
+        if n < 1 or n > N.PF_MAX_CROPS:
+            raise ValueError(f"1..{N.PF_MAX_CROPS} crops per patch")
+        if len(self.p_blur) != n or len(self.p_solarize) != n:
+            self.p_blur = (list(self.p_blur) + [0.5] * n)[:n]
+            self.p_solarize = (list(self.p_solarize) + [0.0] * n)[:n]
+        if self.blur_kernel != 9:
+            raise ValueError("blur kernel is fixed at 9 (DINOv2)")
+        if self.global_size % 8 or self.local_size % 8:
+            raise ValueError("crop sizes must be multiples of 8")
+
+    @property
+    def n_crops(self) -> int:
+        return self.n_global + self.n_local
+
+    def to_c(self) -> N.MultiCropConfig:
+        c = N.MultiCropConfig()
+        c.n_global, c.n_local = self.n_global, self.n_local
+        c.global_size, c.local_size, c.src_size = self.global_size, self.local_size, self.src_size
+        c.blur_kernel = self.blur_kernel
+        c.global_scale[:] = list(self.global_scale)
+        c.local_scale[:] = list(self.local_scale)
+        c.ratio[:] = list(self.ratio)
+        c.p_flip, c.p_jitter, c.p_gray = self.p_flip, self.p_jitter, self.p_gray
+        c.brightness, c.contrast, c.saturation, c.hue = self.brightness, self.contrast, self.saturation, self.hue
+        c.sigma_min, c.sigma_max = self.sigma
+        c.solarize_threshold = self.solarize_threshold
+        for i in range(self.n_crops):
+            c.p_blur[i] = self.p_blur[i]
+            c.p_solarize[i] = self.p_solarize[i]
+        return c
+
+    def bytes_per_patch(self, dtype: str = "bf16") -> int:
+        """Algorithmic HBM bytes per patch: u8 source read once + every crop written once."""
+        el = {"bf16": 2, "f32": 4, "u8": 1}[dtype]
+        out = 3 * el * (self.n_global * self.global_size**2 + self.n_local * self.local_size**2)
+        return 3 * self.src_size**2 + out
+
+
+def crop_params(cfg: MultiCropConfig, n_patches: int, seed: int, rank: int = 0, step: int = 0, out=None, stream=None):
+    """[n_patches, n_crops, 64] uint8 device tensor of pf_crop_param records."""
+    torch = N.require_cuda()
+    if out is None:
+        out = torch.empty((n_patches, cfg.n_crops, 64), dtype=torch.uint8, device="cuda")
+    ccfg = cfg.to_c()
+    N.check(N.lib().pf_crop_params(seed & ((1 << 64) - 1), rank, step, n_patches, C.byref(ccfg), out.data_ptr(),
+                                   N.stream_ptr(stream)), "pf_crop_params")
+    return out
+
+
+def params_host(params_dev) -> np.ndarray:
+    return params_dev.cpu().numpy().reshape(-1, 64).view(N.CROP_DTYPE).reshape(params_dev.shape[:-1])
+
+
+_DT = {"u8": N.PF_U8, "f32": N.PF_F32, "bf16": N.PF_BF16}
+
+
+def multicrop(slide_set, specs_dev, params_dev, cfg: MultiCropConfig, *, dtype: str = "bf16", mean=IMAGENET_MEAN,
+              std=IMAGENET_STD, src_hwc=None, out_global=None, out_local=None, stream=None):
+    """Fused gather + multi-crop -> ([n_global, n, 3, G, G], [n_local, n, 3, L, L]) device tensors."""
+    torch = N.require_cuda()
+    n = int(specs_dev.shape[0])
+    tdt = {"u8": torch.uint8, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+    if out_global is None:
+        out_global = torch.empty((cfg.n_global, n, 3, cfg.global_size, cfg.global_size), dtype=tdt, device="cuda")
+    if out_local is None:
+        out_local = torch.empty((cfg.n_local, n, 3, cfg.local_size, cfg.local_size), dtype=tdt, device="cuda")
+    ccfg = cfg.to_c()
+    m = (C.c_float * 3)(*mean)
+    s = (C.c_float * 3)(*std)
+    N.check(
+        N.lib().pf_multicrop(slide_set.descs.data_ptr(), specs_dev.data_ptr(),
+                             src_hwc.data_ptr() if src_hwc is not None else None, n, params_dev.data_ptr(),
+                             C.byref(ccfg), _DT[dtype], C.cast(m, C.c_void_p), C.cast(s, C.c_void_p),
+                             out_global.data_ptr() if cfg.n_global else None,
+                             out_local.data_ptr() if cfg.n_local else None, N.stream_ptr(stream)),
+        "pf_multicrop",
+    )
+    return out_global, out_local
+
+
+class MultiCropLoader:
+    """Online patching training feed: sampler -> (resample) -> params -> fused multi-crop.
+
+    ``slides``: list of (GpuSlide, ForegroundPolygon).  Each ``next_batch``
+    enqueues the whole step on the current stream and returns device tensors;
+    per-rank streams follow the reference's seed + rank sharding for the
+    coordinates and Philox(seed, rank, step) for the augmentation.
+    """
+
+    def __init__(self, slides, sampler_config, mc_config: MultiCropConfig | None = None, *, batch_size: int = 1024,
+                 rank: int = 0, dtype: str = "bf16", mean=IMAGENET_MEAN, std=IMAGENET_STD, window=None, rounds: int = 4):
+        torch = N.require_cuda()
+        from .sampler import GpuSampler
+        from .store import SlideSet
+
+        self.mc = mc_config or MultiCropConfig()
+        if sampler_config.patch_size != self.mc.src_size:
+            raise ValueError("sampler patch_size must equal the multi-crop source size")
+        self.slide_set = SlideSet([s for s, _ in slides])
+        self.sampler = GpuSampler(sampler_config, slides, slide_set=self.slide_set, window=window, rounds=rounds)
+        self.batch_size = batch_size
+        self.rank = rank
+        self.seed = sampler_config.seed
+        self.dtype = dtype
+        self.mean, self.std = mean, std
+        self.step = 0
+        sides = {int(t.side[k]) for t in _table(self.sampler) for k in range(len(sampler_config.target_mpps))}
+        self.needs_resample = any(sd != self.mc.src_size for sd in sides)
+        S = self.mc.src_size
+        self.specs = torch.empty((batch_size, 64), dtype=torch.uint8, device="cuda")
+        self.params = torch.empty((batch_size, self.mc.n_crops, 64), dtype=torch.uint8, device="cuda")
+        self.src = torch.empty((batch_size, S, S, 3), dtype=torch.uint8, device="cuda") if self.needs_resample else None
+        tdt = {"u8": torch.uint8, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+        self.out_global = torch.empty((self.mc.n_global, batch_size, 3, self.mc.global_size, self.mc.global_size),
+                                      dtype=tdt, device="cuda")
+        self.out_local = torch.empty((self.mc.n_local, batch_size, 3, self.mc.local_size, self.mc.local_size),
+                                     dtype=tdt, device="cuda")
+
+    def next_batch(self, stream=None) -> dict:
+        n = self.batch_size
+        self.sampler.next_batch(n, out=self.specs, stream=stream)
+        if self.needs_resample:
+            m = (C.c_float * 3)(0.5, 0.5, 0.5)
+            N.check(N.lib().pf_read_regions(self.slide_set.descs.data_ptr(), self.specs.data_ptr(), n, self.mc.src_size,
+                                            N.PF_U8, N.PF_HWC | N.PF_SKIP_PASSTHROUGH, C.cast(m, C.c_void_p),
+                                            C.cast(m, C.c_void_p), self.src.data_ptr(), N.stream_ptr(stream)),
+                    "pf_read_regions")
+        crop_params(self.mc, n, self.seed, self.rank, self.step, out=self.params, stream=stream)
+        multicrop(self.slide_set, self.specs, self.params, self.mc, dtype=self.dtype, mean=self.mean, std=self.std,
+                  src_hwc=self.src, out_global=self.out_global, out_local=self.out_local, stream=stream)
+        self.step += 1
+        return {"global_crops": self.out_global, "local_crops": self.out_local, "specs": self.specs,
+                "params": self.params}
+
+    def kernels_per_batch(self) -> int:
+        """CUDA kernels one next_batch launches (sampler rounds + resample + params + 2 multi-crop groups)."""
+        smp = 1 + (2 * self.sampler.rounds if self.sampler.all_fit and self.sampler.rounds > 0 else 1)
+        return smp + (1 if self.needs_resample else 0) + 1 + (self.mc.n_global > 0) + (self.mc.n_local > 0)
+
+
+def _table(sampler):
+    raw = sampler.slides_dev.cpu().numpy().tobytes()
+    size = C.sizeof(N.SamplerSlide)
+    return [N.SamplerSlide.from_buffer_copy(raw[i * size:(i + 1) * size]) for i in range(len(raw) // size)]

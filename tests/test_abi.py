@@ -27,7 +27,7 @@ def native():
 
 def header_symbols():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^(?:int|const char\*|uint64_t)\s+(pf_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|void|const char\*|uint64_t)\s+(pf_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_header(native):
