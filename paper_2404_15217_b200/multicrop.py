@@ -168,18 +168,34 @@ class MultiCropLoader:
         self.out_local = torch.empty((self.mc.n_local, batch_size, 3, self.mc.local_size, self.mc.local_size),
                                      dtype=tdt, device="cuda")
 
-    def next_batch(self, stream=None) -> dict:
+    def next_batch(self, stream=None, marks: list | None = None) -> dict:
+        """Enqueue one step.  ``marks`` (optional list) receives (stage, cuda.Event) pairs recorded
+        on the stream after each stage, for live per-stage timing."""
+        torch = N.require_cuda()
+        st = stream or torch.cuda.current_stream()
+
+        def mark(name):
+            if marks is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(st)
+                marks.append((name, ev))
+
         n = self.batch_size
-        self.sampler.next_batch(n, out=self.specs, stream=stream)
+        mark("begin")
+        self.sampler.next_batch(n, out=self.specs, stream=st)
+        mark("sample")
         if self.needs_resample:
             m = (C.c_float * 3)(0.5, 0.5, 0.5)
             N.check(N.lib().pf_read_regions(self.slide_set.descs.data_ptr(), self.specs.data_ptr(), n, self.mc.src_size,
                                             N.PF_U8, N.PF_HWC | N.PF_SKIP_PASSTHROUGH, C.cast(m, C.c_void_p),
-                                            C.cast(m, C.c_void_p), self.src.data_ptr(), N.stream_ptr(stream)),
+                                            C.cast(m, C.c_void_p), self.src.data_ptr(), N.stream_ptr(st)),
                     "pf_read_regions")
-        crop_params(self.mc, n, self.seed, self.rank, self.step, out=self.params, stream=stream)
+            mark("resample")
+        crop_params(self.mc, n, self.seed, self.rank, self.step, out=self.params, stream=st)
+        mark("params")
         multicrop(self.slide_set, self.specs, self.params, self.mc, dtype=self.dtype, mean=self.mean, std=self.std,
-                  src_hwc=self.src, out_global=self.out_global, out_local=self.out_local, stream=stream)
+                  src_hwc=self.src, out_global=self.out_global, out_local=self.out_local, stream=st)
+        mark("multicrop")
         self.step += 1
         return {"global_crops": self.out_global, "local_crops": self.out_local, "specs": self.specs,
                 "params": self.params}
