@@ -17,6 +17,8 @@
 // and no sequence number, exactly like the reference.  Whenever the
 // assumptions do not hold (a footprint that does not fit, a rejected draw,
 // a window that ran out) the walk continues on the sequential exact path.
+#include <algorithm>
+
 #include "pf_common.cuh"
 #include "pf_poly.cuh"
 
@@ -44,6 +46,7 @@ struct SamplerWs {
     uint32_t* bitmaps;  // [n_slides][window/32]
     int4* cands;        // [n_slides][window]: x, y, mpp_idx, -
     int32_t* reject_at; // first window offset whose coords draws were rejected
+    int2* emits;        // [window]: (slide, window offset) of specs emitted by the walk
 };
 
 __host__ __device__ inline SamplerWs carve_ws(void* ws, int n_slides, int window) {
@@ -54,12 +57,14 @@ __host__ __device__ inline SamplerWs carve_ws(void* ws, int n_slides, int window
     w.bitmaps = reinterpret_cast<uint32_t*>(p);
     p += (((size_t)n_slides * (window / 32) * 4) + 255) / 256 * 256;
     w.cands = reinterpret_cast<int4*>(p);
+    p += (size_t)n_slides * window * 16;
+    w.emits = reinterpret_cast<int2*>(p);
     return w;
 }
 
 __host__ __device__ inline int64_t ws_bytes(int n_slides, int window) {
     return 256 + ((int64_t)n_slides * (window / 32) * 4 + 255) / 256 * 256 +
-           (int64_t)n_slides * window * 16;
+           (int64_t)n_slides * window * 16 + (int64_t)window * 8;
 }
 
 // RandomStream.weighted_index (rng.py:88-103) given the stream draw u.
@@ -233,87 +238,145 @@ __device__ inline int slow_attempt(const pf_sampler_config& cfg, const pf_sample
     return 0;
 }
 
-__global__ void sample_walk_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
-                                   const pf_slide_desc* descs, pf_sampler_state* state, SamplerWs ws,
-                                   int window, int n, int use_table, int finish, pf_patch_spec* out) {
-    extern __shared__ __align__(16) uint32_t s_masks[];
+// Walk with the speculation table: warp 0 consumes slide draws in stream order
+// against the accept bitmaps staged in shared memory; each emitted spec is
+// recorded as (slide, window offset) and materialised afterwards by the whole
+// block.  The exact sequential path finishes whatever the table cannot decide.
+constexpr int kWalkThreads = 256;
+constexpr int kDrawCache = 256;
+
+__global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
+    pf_sampler_config cfg, const pf_sampler_slide* slides, const pf_slide_desc* descs, pf_sampler_state* state,
+    SamplerWs ws, int window, int n, int use_table, int finish, int bitmaps_in_smem, int2* emit_list,
+    pf_patch_spec* out) {
+    extern __shared__ __align__(16) uint32_t s_dyn[];
+    __shared__ int16_t s_draw[kDrawCache];
+    __shared__ int s_first, s_last;
     WalkState w;
     load_ws(state, w);
     if (w.status != PF_OK || w.emitted >= n) return;
-    const int lane = threadIdx.x & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int max_att = cfg.max_attempts;
     const int64_t flimit = failure_limit(cfg);
+    const int words = window / 32;
+    if (tid == 0) {
+        s_first = w.emitted;
+        s_last = w.emitted;
+    }
     if (use_table) {
-        const uint64_t m0 = w.c_mpp, c0 = w.c_coords;
-        const int wlim = min(window, *ws.reject_at);
-        const int words = window / 32;
-        while (w.emitted < n && w.status == PF_OK) {
-            if (w.cur_slide < 0) {
-                w.cur_slide = draw_slide(cfg, slides, w.c_slide);
-                w.cur_used = 0;
-            }
-            const int a0 = (int)(w.c_mpp - m0);
-            const int budget = max_att - w.cur_used;
-            const int avail = wlim - a0;
-            const int span = min(budget, avail);
-            // first accepted attempt of slide cur_slide in [a0, a0 + span)
-            int found = -1;
-            if (span > 0) {
-                const uint32_t* bm = ws.bitmaps + (size_t)w.cur_slide * words;
-                const int wfirst = a0 >> 5, wlast = (a0 + span - 1) >> 5;
-                for (int base = wfirst; base <= wlast && found < 0; base += 32) {
-                    const int wi = base + lane;
-                    uint32_t bits = 0;
-                    if (wi <= wlast) {
-                        bits = bm[wi];
-                        if (wi == wfirst) bits &= 0xffffffffu << (a0 & 31);
-                        if (wi == wlast) {
-                            const int e = (a0 + span - 1) & 31;
-                            bits &= (e == 31) ? 0xffffffffu : ((1u << (e + 1)) - 1u);
+        const uint32_t* bm_all = ws.bitmaps;
+        if (bitmaps_in_smem) {
+            for (int i = tid; i < cfg.n_slides * words; i += kWalkThreads) s_dyn[i] = ws.bitmaps[i];
+            bm_all = s_dyn;
+        }
+        __syncthreads();
+        if (tid < 32) {
+            const uint64_t m0 = w.c_mpp;
+            const int wlim = min(window, *ws.reject_at);
+            int draw_pos = kDrawCache, draw_cnt = kDrawCache;
+            uint64_t draw_base = w.c_slide;  // counter of s_draw[0] is draw_base + 1
+            while (w.emitted < n && w.status == PF_OK) {
+                if (w.cur_slide < 0) {
+                    if (draw_pos == draw_cnt) {  // refill: 32 lanes draw the next kDrawCache counters
+                        draw_base = w.c_slide;
+                        for (int i = lane; i < kDrawCache; i += 32) {
+                            const uint64_t v = stream_u64(cfg.key_slide, draw_base + 1 + (uint64_t)i);
+                            int sidx;
+                            if (cfg.strategy == 0) {
+                                const uint64_t nn = (uint64_t)cfg.n_slides;
+                                sidx = randrange_accepts(v, randrange_limit(nn)) ? (int)(v % nn) : -1;
+                            } else {
+                                double total = 0.0;
+                                for (int k = 0; k < cfg.n_slides; ++k) total = __dadd_rn(total, slides[k].weight);
+                                const double u = __dadd_rn(0.0, __dmul_rn(u64_to_unit(v), __dsub_rn(total, 0.0)));
+                                double acc = 0.0;
+                                sidx = cfg.n_slides - 1;
+                                for (int k = 0; k < cfg.n_slides; ++k) {
+                                    acc = __dadd_rn(acc, slides[k].weight);
+                                    if (u < acc) {
+                                        sidx = k;
+                                        break;
+                                    }
+                                }
+                            }
+                            s_draw[i] = (int16_t)sidx;
+                        }
+                        __syncwarp();
+                        draw_pos = 0;
+                    }
+                    const int sidx = s_draw[draw_pos++];
+                    w.c_slide += 1;
+                    if (sidx < 0) continue;  // rejected draw: randrange retries with the next counter
+                    w.cur_slide = sidx;
+                    w.cur_used = 0;
+                }
+                const int a0 = (int)(w.c_mpp - m0);
+                const int budget = max_att - w.cur_used;
+                const int span = min(budget, wlim - a0);
+                int found = -1;
+                if (span > 0) {
+                    const uint32_t* bm = bm_all + (size_t)w.cur_slide * words;
+                    const int wfirst = a0 >> 5, wlast = (a0 + span - 1) >> 5;
+                    for (int base = wfirst; base <= wlast && found < 0; base += 32) {
+                        const int wi = base + lane;
+                        uint32_t bits = 0;
+                        if (wi <= wlast) {
+                            bits = bm[wi];
+                            if (wi == wfirst) bits &= 0xffffffffu << (a0 & 31);
+                            if (wi == wlast) {
+                                const int e = (a0 + span - 1) & 31;
+                                bits &= (e == 31) ? 0xffffffffu : ((1u << (e + 1)) - 1u);
+                            }
+                        }
+                        const uint32_t ball = __ballot_sync(0xffffffffu, bits != 0);
+                        if (ball) {
+                            const int src = __ffs(ball) - 1;
+                            const uint32_t b = __shfl_sync(0xffffffffu, bits, src);
+                            found = (base + src) * 32 + __ffs(b) - 1;
                         }
                     }
-                    const uint32_t ball = __ballot_sync(0xffffffffu, bits != 0);
-                    if (ball) {
-                        const int src = __ffs(ball) - 1;
-                        const uint32_t b = __shfl_sync(0xffffffffu, bits, src);
-                        found = (base + src) * 32 + __ffs(b) - 1;
-                    }
+                }
+                if (found >= 0) {
+                    const int consumed = found - a0 + 1;
+                    w.c_mpp += consumed;
+                    w.c_coords += 2ull * consumed;
+                    w.attempts += consumed;
+                    if (lane == 0) emit_list[w.emitted - s_first] = make_int2(w.cur_slide, found);  // < window per round
+                    w.seq += 1;
+                    w.emitted += 1;
+                    w.failures = 0;
+                    w.cur_slide = -1;
+                } else if (span == budget) {
+                    w.c_mpp += span;  // ExhaustedAttemptsError: redraw, no seq consumed
+                    w.c_coords += 2ull * span;
+                    w.attempts += span;
+                    w.cur_slide = -1;
+                    w.failures += 1;
+                    if (w.failures >= flimit) w.status = PF_ERR_NO_SAMPLABLE;
+                } else {
+                    w.c_mpp += span;  // window (or a rejected draw) reached
+                    w.c_coords += 2ull * span;
+                    w.attempts += span;
+                    w.cur_used += span;
+                    break;
                 }
             }
-            if (found >= 0) {
-                const int consumed = found - a0 + 1;
-                w.c_mpp += consumed;
-                w.c_coords += 2ull * consumed;
-                w.attempts += consumed;
-                if (lane == 0) {
-                    const int4 cd = ws.cands[(size_t)w.cur_slide * window + found];
-                    emit_spec(cfg, slides[w.cur_slide], descs[w.cur_slide], w.cur_slide, cd.x, cd.y, cd.z,
-                              w.seq, out + w.emitted);
-                }
-                w.seq += 1;
-                w.emitted += 1;
-                w.failures = 0;
-                w.cur_slide = -1;
-            } else if (span == budget) {
-                // exhausted this slide draw (ExhaustedAttemptsError)
-                w.c_mpp += span;
-                w.c_coords += 2ull * span;
-                w.attempts += span;
-                w.cur_slide = -1;
-                w.failures += 1;
-                if (w.failures >= flimit) w.status = PF_ERR_NO_SAMPLABLE;
-            } else {
-                // window (or a rejected draw) reached: consume what was seen
-                w.c_mpp += span;
-                w.c_coords += 2ull * span;
-                w.attempts += span;
-                w.cur_used += span;
-                break;
-            }
+            // unused precomputed draws were never consumed: c_slide already counts only consumed ones
+            if (lane == 0) s_last = w.emitted;
+        }
+        __syncthreads();
+        // materialise the emitted specs in parallel
+        const int first = s_first, last = s_last;
+        const int64_t seq0 = state->seq;
+        for (int i = first + tid; i < last; i += kWalkThreads) {
+            const int2 e = emit_list[i - first];
+            const int4 cd = ws.cands[(size_t)e.x * window + e.y];
+            emit_spec(cfg, slides[e.x], descs[e.x], e.x, cd.x, cd.y, cd.z, seq0 + (i - first), out + i);
         }
     }
+    if (tid >= 32) return;
     if (finish) {
-        uint32_t* sm = s_masks;
+        uint32_t* sm = s_dyn;
         while (w.emitted < n && w.status == PF_OK) {
             if (w.cur_slide < 0) {
                 w.cur_slide = draw_slide(cfg, slides, w.c_slide);
@@ -384,7 +447,12 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     if (rc) return rc;
     const int warps = 8;
     const size_t eval_smem = (size_t)warps * overlap_smem_bytes(cfg->grid);
-    const size_t walk_smem = overlap_smem_bytes(cfg->grid);
+    const size_t bm_bytes_all = (size_t)cfg->n_slides * (window / 32) * 4;
+    const int bm_in_smem = rounds > 0 && bm_bytes_all <= 160 * 1024;
+    const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid), bm_in_smem ? bm_bytes_all : (size_t)0);
+    rc = check_cuda(cudaFuncSetAttribute(sample_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)walk_smem),
+                    "cudaFuncSetAttribute");
+    if (rc) return rc;
     rc = check_cuda(cudaFuncSetAttribute(sample_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)eval_smem), "cudaFuncSetAttribute");
     if (rc) return rc;
@@ -400,13 +468,14 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
         const int64_t blocks = (cands + warps - 1) / warps;
         sample_eval_kernel<<<(unsigned)blocks, warps * 32, eval_smem, st>>>(*cfg, slides_dev, state_dev, ws, window, n);
         if ((rc = after_launch("sample_eval_kernel"))) return rc;
-        sample_walk_kernel<<<1, 32, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws, window, n, 1,
-                                                     r == rounds - 1, out_dev);
+        sample_walk_kernel<<<1, kWalkThreads, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws,
+                                                                window, n, 1, r == rounds - 1, bm_in_smem,
+                                                                ws.emits, out_dev);
         if ((rc = after_launch("sample_walk_kernel"))) return rc;
     }
     if (rounds == 0) {
-        sample_walk_kernel<<<1, 32, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws, window, n, 0, 1,
-                                                     out_dev);
+        sample_walk_kernel<<<1, kWalkThreads, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws,
+                                                                window, n, 0, 1, 0, nullptr, out_dev);
         if ((rc = after_launch("sample_walk_kernel"))) return rc;
     }
     return PF_OK;
