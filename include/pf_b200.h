@@ -245,6 +245,8 @@ int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* slides_dev,
 /* Multi-crop augmentation (BASELINE config 2; absent from the reference)    */
 /* ------------------------------------------------------------------------ */
 typedef struct pf_multicrop_config {
+    uint64_t rrc_table_global;        /* device pf_rrc_table for global_size (0: computed per crop) */
+    uint64_t rrc_table_local;         /* device pf_rrc_table for local_size  (0: computed per crop) */
     int32_t n_global, n_local;
     int32_t global_size, local_size;
     int32_t src_size;                 /* source patch side (224) */
@@ -282,6 +284,13 @@ typedef struct pf_crop_param {
  * n_patches * (n_global + n_local) records, patch-major. */
 int pf_crop_params(uint64_t seed, int32_t rank, uint64_t step, int32_t n_patches,
                    const pf_multicrop_config* cfg, pf_crop_param* out_dev, void* stream);
+
+/* RandomResizedCrop resample taps for every crop extent 1..src_size to
+ * out_size: torch uint8 antialiased bilinear (int16 weights, per-extent
+ * precision), as used by torchvision resized_crop.  Built once on device;
+ * pass its address in pf_multicrop_config.rrc_table_*. */
+int pf_rrc_table_bytes(int32_t src_size, int32_t out_size, int64_t* bytes);
+int pf_rrc_table_build(int32_t src_size, int32_t out_size, void* table_dev, void* stream);
 
 /* One Philox4x32-10 block (Random123 semantics): out = philox(ctr, key). */
 void pf_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

@@ -109,6 +109,8 @@ class SamplerState(C.Structure):
 
 class MultiCropConfig(C.Structure):
     _fields_ = [
+        ("rrc_table_global", C.c_uint64),
+        ("rrc_table_local", C.c_uint64),
         ("n_global", C.c_int32),
         ("n_local", C.c_int32),
         ("global_size", C.c_int32),
@@ -197,6 +199,8 @@ class _Lib:
                 C.c_int,
             ),
             "pf_philox4x32_10": ([vp, vp, vp], None),
+            "pf_rrc_table_bytes": ([i32, i32, C.POINTER(i64)], C.c_int),
+            "pf_rrc_table_build": ([i32, i32, vp, vp], C.c_int),
             "pf_synth_level0": ([C.POINTER(SlideDesc), vp, i32, i32, i32, C.c_float, u64, vp], C.c_int),
         }
         self.symbols = sorted(sig)

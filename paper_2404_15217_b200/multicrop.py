@@ -64,8 +64,11 @@ class MultiCropConfig:
     def n_crops(self) -> int:
         return self.n_global + self.n_local
 
-    def to_c(self) -> N.MultiCropConfig:
+    def to_c(self, with_tables: bool = True) -> N.MultiCropConfig:
         c = N.MultiCropConfig()
+        if with_tables:
+            c.rrc_table_global = rrc_table(self.src_size, self.global_size)
+            c.rrc_table_local = rrc_table(self.src_size, self.local_size)
         c.n_global, c.n_local = self.n_global, self.n_local
         c.global_size, c.local_size, c.src_size = self.global_size, self.local_size, self.src_size
         c.blur_kernel = self.blur_kernel
@@ -88,12 +91,30 @@ class MultiCropConfig:
         return 3 * self.src_size**2 + out
 
 
+_RRC_TABLES: dict = {}
+
+
+def rrc_table(src_size: int, out_size: int) -> int:
+    """Device address of the RandomResizedCrop tap table for (src_size -> out_size), built once
+    per process (pf_rrc_table_build) and kept alive here."""
+    key = (src_size, out_size)
+    t = _RRC_TABLES.get(key)
+    if t is None:
+        torch = N.require_cuda()
+        nbytes = C.c_int64(0)
+        N.check(N.lib().pf_rrc_table_bytes(src_size, out_size, C.byref(nbytes)), "pf_rrc_table_bytes")
+        t = torch.empty((nbytes.value,), dtype=torch.uint8, device="cuda")
+        N.check(N.lib().pf_rrc_table_build(src_size, out_size, t.data_ptr(), N.stream_ptr()), "pf_rrc_table_build")
+        _RRC_TABLES[key] = t
+    return int(t.data_ptr())
+
+
 def crop_params(cfg: MultiCropConfig, n_patches: int, seed: int, rank: int = 0, step: int = 0, out=None, stream=None):
     """[n_patches, n_crops, 64] uint8 device tensor of pf_crop_param records."""
     torch = N.require_cuda()
     if out is None:
         out = torch.empty((n_patches, cfg.n_crops, 64), dtype=torch.uint8, device="cuda")
-    ccfg = cfg.to_c()
+    ccfg = cfg.to_c(with_tables=False)
     N.check(N.lib().pf_crop_params(seed & ((1 << 64) - 1), rank, step, n_patches, C.byref(ccfg), out.data_ptr(),
                                    N.stream_ptr(stream)), "pf_crop_params")
     return out
