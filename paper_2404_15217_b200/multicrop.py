@@ -161,7 +161,8 @@ class MultiCropLoader:
     """
 
     def __init__(self, slides, sampler_config, mc_config: MultiCropConfig | None = None, *, batch_size: int = 1024,
-                 rank: int = 0, dtype: str = "bf16", mean=IMAGENET_MEAN, std=IMAGENET_STD, window=None, rounds: int = 4):
+                 rank: int = 0, dtype: str = "bf16", mean=IMAGENET_MEAN, std=IMAGENET_STD, window=None, rounds: int = 4,
+                 prefetch: bool = True):
         torch = N.require_cuda()
         from .sampler import GpuSampler
         from .store import SlideSet
@@ -180,7 +181,12 @@ class MultiCropLoader:
         sides = {int(t.side[k]) for t in _table(self.sampler) for k in range(len(sampler_config.target_mpps))}
         self.needs_resample = any(sd != self.mc.src_size for sd in sides)
         S = self.mc.src_size
-        self.specs = torch.empty((batch_size, 64), dtype=torch.uint8, device="cuda")
+        self.specs_slots = [torch.empty((batch_size, 64), dtype=torch.uint8, device="cuda") for _ in range(2)]
+        self.prefetch = prefetch
+        self._side = torch.cuda.Stream()
+        self._ready = [None, None]
+        self._free = [torch.cuda.Event(), torch.cuda.Event()]
+        self._next_slot = 0
         self.params = torch.empty((batch_size, self.mc.n_crops, 64), dtype=torch.uint8, device="cuda")
         self.src = torch.empty((batch_size, S, S, 3), dtype=torch.uint8, device="cuda") if self.needs_resample else None
         tdt = {"u8": torch.uint8, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
@@ -189,9 +195,16 @@ class MultiCropLoader:
         self.out_local = torch.empty((self.mc.n_local, batch_size, 3, self.mc.local_size, self.mc.local_size),
                                      dtype=tdt, device="cuda")
 
+    def _sample(self, slot: int, st) -> None:
+        self.sampler.next_batch(self.batch_size, out=self.specs_slots[slot], stream=st)
+
     def next_batch(self, stream=None, marks: list | None = None) -> dict:
-        """Enqueue one step.  ``marks`` (optional list) receives (stage, cuda.Event) pairs recorded
-        on the stream after each stage, for live per-stage timing."""
+        """Enqueue one step and return its device tensors.
+
+        With ``prefetch`` (default) the specs of step k+1 are sampled on a side stream while
+        step k's crops are computed: the sampler's serial walk overlaps the previous batch's
+        multi-crop instead of idling the GPU in front of it.  ``marks`` (optional list) receives
+        (stage, cuda.Event) pairs recorded on the main stream after each stage."""
         torch = N.require_cuda()
         st = stream or torch.cuda.current_stream()
 
@@ -203,23 +216,48 @@ class MultiCropLoader:
 
         n = self.batch_size
         mark("begin")
-        self.sampler.next_batch(n, out=self.specs, stream=st)
-        mark("sample")
+        if not self.prefetch:
+            self._sample(0, st)
+            cur = 0
+            mark("sample")
+        else:
+            cur = self._next_slot
+            if self._ready[cur] is None:  # first step: nothing prefetched yet
+                self._side.wait_stream(st)
+                self._sample(cur, self._side)
+                self._ready[cur] = torch.cuda.Event()
+                self._ready[cur].record(self._side)
+            st.wait_event(self._ready[cur])
+            mark("sample_wait")
+            nxt = 1 - cur
+            self._side.wait_event(self._free[nxt])  # step k-1 finished reading that slot
+            self._sample(nxt, self._side)
+            self._ready[nxt] = torch.cuda.Event()
+            self._ready[nxt].record(self._side)
+            self._next_slot = nxt
+        specs = self.specs_slots[cur]
         if self.needs_resample:
             m = (C.c_float * 3)(0.5, 0.5, 0.5)
-            N.check(N.lib().pf_read_regions(self.slide_set.descs.data_ptr(), self.specs.data_ptr(), n, self.mc.src_size,
+            N.check(N.lib().pf_read_regions(self.slide_set.descs.data_ptr(), specs.data_ptr(), n, self.mc.src_size,
                                             N.PF_U8, N.PF_HWC | N.PF_SKIP_PASSTHROUGH, C.cast(m, C.c_void_p),
                                             C.cast(m, C.c_void_p), self.src.data_ptr(), N.stream_ptr(st)),
                     "pf_read_regions")
             mark("resample")
         crop_params(self.mc, n, self.seed, self.rank, self.step, out=self.params, stream=st)
         mark("params")
-        multicrop(self.slide_set, self.specs, self.params, self.mc, dtype=self.dtype, mean=self.mean, std=self.std,
+        multicrop(self.slide_set, specs, self.params, self.mc, dtype=self.dtype, mean=self.mean, std=self.std,
                   src_hwc=self.src, out_global=self.out_global, out_local=self.out_local, stream=st)
         mark("multicrop")
+        if self.prefetch:
+            self._free[cur].record(st)
         self.step += 1
-        return {"global_crops": self.out_global, "local_crops": self.out_local, "specs": self.specs,
+        return {"global_crops": self.out_global, "local_crops": self.out_local, "specs": specs,
                 "params": self.params}
+
+    def drain(self) -> None:
+        """Wait for the prefetched sampler work (so the sampler state is final)."""
+        torch = N.require_cuda()
+        torch.cuda.current_stream().wait_stream(self._side)
 
     def kernels_per_batch(self) -> int:
         """CUDA kernels one next_batch launches (sampler rounds + resample + params + 2 multi-crop groups)."""

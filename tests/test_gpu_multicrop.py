@@ -132,6 +132,13 @@ def test_loader_end_to_end(pf):
     out = loader.next_batch()
     out2 = loader.next_batch()
     assert out["global_crops"].shape == (2, 32, 3, 224, 224) and out["local_crops"].shape == (8, 32, 3, 96, 96)
+    torch = pytest.importorskip("torch")
+    torch.cuda.synchronize()
     st = loader.sampler.check()
-    assert st.seq == 64
+    assert st.seq == 3 * 32  # two consumed batches + one prefetched
+    # the prefetched stream is the plain stream: same specs as sampling without prefetch
+    ref = pf.mc.MultiCropLoader([(s, poly)], cfg, batch_size=32, prefetch=False)
+    ref.next_batch()
+    b2 = ref.next_batch()
+    assert torch.equal(b2["specs"], out2["specs"]) and torch.equal(b2["global_crops"], out2["global_crops"])
     assert bool(out2["global_crops"].float().abs().sum() > 0)
