@@ -128,17 +128,21 @@ def build_workload(args, rank, torch):
     from paper_2404_15217_b200.multicrop import MultiCropConfig, MultiCropLoader
     from paper_2404_15217_b200.synthetic import synthetic_slide
 
+    from paper_2404_15217_b200.shard import rank_plan
+
+    world = dist_env()[1]
+    plan = rank_plan(rank, world, args.slides * world, seed=0)  # rank r owns slides [16r, 16r+16)
     slides = []
-    for i in range(args.slides):
-        sid = f"r{rank}s{i}"
-        s = synthetic_slide(sid, args.width, args.height, seed=1000 * rank + i, downsample_factor=4)
+    for gi in plan.slide_indices:
+        sid = f"s{gi}"
+        s = synthetic_slide(sid, args.width, args.height, seed=1000 + gi, downsample_factor=4)
         thumb, scale = s.thumbnail_device(32)
         mask = pf.foreground.mask_device(thumb, 1, 0.07, 1)  # BASELINE: saturation > 0.07 + morphology
         bm = pf.BinaryMask(mask.cpu().numpy().astype(bool), scale)
         poly = pf.polygon_from_mask(bm, slide_id=sid)
         slides.append((s, poly))
     mpps = [(0.25, 1.0), (0.5, 1.0), (1.0, 1.0), (2.0, 1.0)] if args.mixed_mpp else [(0.25, 1.0)]
-    scfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=mpps, seed=pf.rng.shard_seed(0, rank))
+    scfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=mpps, seed=plan.sampler_seed)
     mc = MultiCropConfig()
     loader = MultiCropLoader(slides, scfg, mc, batch_size=args.batch, rank=rank, dtype=args.dtype)
     return pf, slides, loader, mc
