@@ -39,16 +39,35 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--batch", type=int, default=1024)
-    ap.add_argument("--slides", type=int, default=16)
-    ap.add_argument("--width", type=int, default=40000)
-    ap.add_argument("--height", type=int, default=30000)
-    ap.add_argument("--mixed-mpp", action="store_true", help="config 3: target mpp U{0.25,0.5,1,2}")
-    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--config", default="2", choices=["1", "2", "3", "5"],
+                    help="BASELINE config: 1 normalise-only, 2 multi-crop (default), 3 mixed mpp, 5 sweep")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--slides", type=int, default=None)
+    ap.add_argument("--width", type=int, default=None)
+    ap.add_argument("--height", type=int, default=None)
+    ap.add_argument("--mixed-mpp", action="store_true", help="same as --config 3")
+    ap.add_argument("--dtype", default=None, choices=["bf16", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.mixed_mpp:
+        args.config = "3"
+    base = CONFIGS[args.config]
+    for k in ("batch", "slides", "width", "height", "dtype"):
+        if getattr(args, k) is None:
+            setattr(args, k, base[k])
+    args.mixed_mpp = args.config == "3"
+    return args
+
+
+# BASELINE.json configs (per GPU)
+CONFIGS = {
+    "1": dict(batch=256, slides=1, width=8192, height=8192, dtype="f32"),
+    "2": dict(batch=1024, slides=16, width=40000, height=30000, dtype="bf16"),
+    "3": dict(batch=2048, slides=16, width=40000, height=30000, dtype="bf16"),
+    "5": dict(batch=1024, slides=1, width=100000, height=80000, dtype="bf16"),
+}
 
 
 def dist_env():
@@ -123,14 +142,13 @@ class ClockSampler:
 # B200 arm
 
 
-def build_workload(args, rank, torch):
+def build_slides(args, rank, world):
+    """Render this rank's slides in HBM, threshold the BASELINE saturation mask on the 1/32
+    thumbnail and trace each slide's foreground polygon."""
     import paper_2404_15217_b200 as pf
-    from paper_2404_15217_b200.multicrop import MultiCropConfig, MultiCropLoader
+    from paper_2404_15217_b200.shard import rank_plan
     from paper_2404_15217_b200.synthetic import synthetic_slide
 
-    from paper_2404_15217_b200.shard import rank_plan
-
-    world = dist_env()[1]
     plan = rank_plan(rank, world, args.slides * world, seed=0)  # rank r owns slides [16r, 16r+16)
     slides = []
     for gi in plan.slide_indices:
@@ -139,30 +157,61 @@ def build_workload(args, rank, torch):
         thumb, scale = s.thumbnail_device(32)
         mask = pf.foreground.mask_device(thumb, 1, 0.07, 1)  # BASELINE: saturation > 0.07 + morphology
         bm = pf.BinaryMask(mask.cpu().numpy().astype(bool), scale)
-        poly = pf.polygon_from_mask(bm, slide_id=sid)
-        slides.append((s, poly))
-    mpps = [(0.25, 1.0), (0.5, 1.0), (1.0, 1.0), (2.0, 1.0)] if args.mixed_mpp else [(0.25, 1.0)]
+        slides.append((s, pf.polygon_from_mask(bm, slide_id=sid)))
+    return pf, plan, slides
+
+
+class Feed:
+    """One benchmark workload: a loader plus what the roofline needs to know about it."""
+
+    def __init__(self, loader, stage: str, bytes_per_patch: int, kernel: str, workload: str, e2e_fn):
+        self.loader, self.stage, self.bytes_per_patch = loader, stage, bytes_per_patch
+        self.kernel, self.workload, self.e2e_fn = kernel, workload, e2e_fn
+
+    @property
+    def sampler(self):
+        return self.loader.sampler
+
+
+def make_feed(args, pf, plan, slides, rank, src_size=224, n_local=8, patch=224):
+    from paper_2404_15217_b200.multicrop import MultiCropConfig, MultiCropLoader
+    from paper_2404_15217_b200.pipeline import RegionLoader
+
+    if args.config == "1":
+        scfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=[(0.25, 1.0)], seed=plan.sampler_seed)
+        loader = RegionLoader(slides, scfg, batch_size=args.batch, dtype=args.dtype)
+        el = 4 if args.dtype == "f32" else 2
+        bpp = 224 * 224 * 3 + 224 * 224 * 3 * el
+        wl = (f"C1: {args.slides} slide {args.width}x{args.height} in HBM, sat>0.07+morph mask on 1/32 thumbnail, "
+              f"epoch_stream sampler 224px min_fg 0.40, read_region + ImageNet normalise to {args.dtype} NCHW")
+        return Feed(loader, "read", bpp, "read_regions_kernel", wl, run_e2e_regions)
+    mpps = [(0.25, 1.0), (0.5, 1.0), (1.0, 1.0), (2.0, 1.0)] if args.config == "3" else [(0.25, 1.0)]
+    if args.config == "5":
+        mpps = [(0.25 * patch / 224.0, 1.0)]
     scfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=mpps, seed=plan.sampler_seed)
-    mc = MultiCropConfig()
+    mc = MultiCropConfig(n_local=n_local)
     loader = MultiCropLoader(slides, scfg, mc, batch_size=args.batch, rank=rank, dtype=args.dtype)
-    return pf, slides, loader, mc
+    tag = {"2": "C2", "3": "C3 (mpp U{0.25,0.5,1,2})", "5": f"C5 point (patch {patch}->224, L={n_local})"}[args.config]
+    wl = (f"{tag}: {args.slides} slides {args.width}x{args.height} per GPU in HBM, sat>0.07+morph mask on 1/32 "
+          f"thumbnail, epoch_stream sampler 224px min_fg 0.40, DINOv2 multi-crop 2x224 + {n_local}x96 {args.dtype} NCHW")
+    return Feed(loader, "multicrop", mc.bytes_per_patch(args.dtype), "multicrop_kernel (global + local crop launches)",
+                wl, run_e2e_multicrop)
 
 
-def run_e2e(pf, loader, mc, steps, torch):
+def run_e2e_multicrop(pf, loader, steps, torch):
     """Reference-facing path with HOST buffers: pinned host specs -> H2D -> crop params -> fused
     multi-crop -> D2H of the whole batch into pinned host memory, double-buffered on two streams."""
-    from paper_2404_15217_b200 import _native as N
     from paper_2404_15217_b200.multicrop import crop_params, multicrop
 
+    mc = loader.mc
     n = loader.batch_size
+    loader.drain()
     # a manifest of specs, as a host caller would hold it (run_loader / `patchforge load` input)
-    host_specs = []
-    for _ in range(2):
-        host_specs.append(loader.sampler.next_batch(n).cpu().pin_memory())
+    host_specs = [loader.sampler.next_batch(n).cpu().pin_memory() for _ in range(2)]
     tdt = loader.out_global.dtype
     G, Lc = mc.n_global, mc.n_local
     bufs = []
-    for k in range(2):
+    for _ in range(2):
         bufs.append({
             "specs": torch.empty((n, 64), dtype=torch.uint8, device="cuda"),
             "params": torch.empty((n, mc.n_crops, 64), dtype=torch.uint8, device="cuda"),
@@ -172,8 +221,7 @@ def run_e2e(pf, loader, mc, steps, torch):
             "hl": torch.empty((Lc, n, 3, mc.local_size, mc.local_size), dtype=tdt).pin_memory(),
             "done": torch.cuda.Event(),
         })
-    comp = torch.cuda.Stream()
-    copy = torch.cuda.Stream()
+    comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
     src = loader.src
 
     def step(i):
@@ -191,9 +239,44 @@ def run_e2e(pf, loader, mc, steps, torch):
         with torch.cuda.stream(copy):
             copy.wait_event(ev)
             b["hg"].copy_(b["g"], non_blocking=True)
-            b["hl"].copy_(b["l"], non_blocking=True)
+            if Lc:
+                b["hl"].copy_(b["l"], non_blocking=True)
             b["done"].record(copy)
 
+    return _time_e2e(step, steps, n, torch, n * 64,
+                     bufs[0]["hg"].numel() * bufs[0]["hg"].element_size() + bufs[0]["hl"].numel() * bufs[0]["hl"].element_size(),
+                     "pinned host specs -> pf_crop_params/pf_multicrop -> pinned host crops, 2 streams double-buffered")
+
+
+def run_e2e_regions(pf, loader, steps, torch):
+    """Pinned host specs -> H2D -> pf_read_regions (normalising epilogue) -> D2H of the batch."""
+    n = loader.batch_size
+    torch.cuda.synchronize()
+    host_specs = [loader.sampler.next_batch(n).cpu().pin_memory() for _ in range(2)]
+    bufs = [{"specs": torch.empty((n, 64), dtype=torch.uint8, device="cuda"), "out": torch.empty_like(loader.out),
+             "host": torch.empty(loader.out.shape, dtype=loader.out.dtype).pin_memory(), "done": torch.cuda.Event()}
+            for _ in range(2)]
+    comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def step(i):
+        b = bufs[i % 2]
+        with torch.cuda.stream(comp):
+            comp.wait_event(b["done"])
+            b["specs"].copy_(host_specs[i % 2], non_blocking=True)
+            loader.slide_set.read_regions(b["specs"], loader.out_size, dtype=loader.dtype, layout=loader.layout,
+                                          mean=loader.mean, std=loader.std, out=b["out"], stream=comp, planned=True)
+            ev = torch.cuda.Event()
+            ev.record(comp)
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev)
+            b["host"].copy_(b["out"], non_blocking=True)
+            b["done"].record(copy)
+
+    return _time_e2e(step, steps, n, torch, n * 64, bufs[0]["host"].numel() * bufs[0]["host"].element_size(),
+                     "pinned host specs -> pf_read_regions -> pinned host patches, 2 streams double-buffered")
+
+
+def _time_e2e(step, steps, n, torch, h2d, d2h, path):
     for i in range(2):
         step(i)
     torch.cuda.synchronize()
@@ -202,24 +285,13 @@ def run_e2e(pf, loader, mc, steps, torch):
         step(i)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    out_bytes = sum(b["hg"].numel() * b["hg"].element_size() + b["hl"].numel() * b["hl"].element_size()
-                    for b in bufs[:1])
-    return {"value": steps * n / dt, "unit": "patches/s", "h2d_bytes_per_step": n * 64,
-            "d2h_bytes_per_step": int(out_bytes), "path": "pinned host specs -> pf_crop_params/pf_multicrop -> "
-            "pinned host crops, 2 streams double-buffered; wall clock over the steps"}
+    return {"value": round(steps * n / dt, 1), "unit": "patches/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "path": path + "; wall clock over the steps"}
 
 
-def run_b200(args):
-    import torch
-    import torch.distributed as dist
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    pf, slides, loader, mc = build_workload(args, rank, torch)
-    from paper_2404_15217_b200 import _native as N
-
+def timed_run(feed, args, torch, dist, world, local, N):
+    """W warm-up steps, then K timed steps between barriers; per-stage CUDA events."""
+    loader = feed.loader
     clk = ClockSampler(local).__enter__()  # sampling spans warm-up + timed steps (all under load)
     for _ in range(max(args.warmup, 0)):
         loader.next_batch()
@@ -231,49 +303,106 @@ def run_b200(args):
     stream = torch.cuda.current_stream()
     marks_all = []
     l0 = N.launches()
-    if True:
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.nvtx.range_push("timed")
-        start.record(stream)
-        for _ in range(args.steps):
-            marks = []
-            loader.next_batch(marks=marks)
-            marks_all.append(marks)
-        end.record(stream)
-        torch.cuda.nvtx.range_pop()
-        torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")
+    start.record(stream)
+    for _ in range(args.steps):
+        marks = []
+        loader.next_batch(marks=marks)
+        marks_all.append(marks)
+    end.record(stream)
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
     clk.__exit__(None, None, None)
     launches = N.launches() - l0
     elapsed_ms = start.elapsed_time(end)
-    st = loader.sampler.check()
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
-    elapsed_ms = float(t.item())
     stages: dict = {}
     for marks in marks_all:
-        for (a, ea), (b, eb) in zip(marks[:-1], marks[1:]):
+        for (_, ea), (b, eb) in zip(marks[:-1], marks[1:]):
             stages.setdefault(b, []).append(ea.elapsed_time(eb))
     stage_ms = {k: sum(v) / len(v) for k, v in stages.items()}
+    return float(t.item()), stage_ms, launches, clk.summary()
+
+
+def result_line(feed, args, world, elapsed_ms, stage_ms, launches, clocks, st, e2e, cpu):
+    peak, peak_kind = measured_peak_hbm()
     n_total = args.steps * args.batch * world
     value = n_total / (elapsed_ms / 1000.0)
-    peak, peak_kind = measured_peak_hbm()
-    bpp = mc.bytes_per_patch(args.dtype)
-    mc_ms = stage_ms["multicrop"]
-    achieved = bpp * args.batch / (mc_ms / 1000.0) / 1e9
+    k_ms = stage_ms[feed.stage]
+    achieved = feed.bytes_per_patch * args.batch / (k_ms / 1000.0) / 1e9
     traffic = None
-    tp = ROOT / "profiles" / "multicrop_traffic.json"
+    tp = ROOT / "profiles" / f"traffic_config{args.config}.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get("dram_bytes_per_patch")
-            traffic = traffic * args.batch if traffic else None
+            tpp = json.loads(tp.read_text()).get("dram_bytes_per_patch")
+            traffic = int(tpp * args.batch) if tpp else None
         except Exception:  # noqa: BLE001
             traffic = None
-    clocks = clk.summary()
+    return {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "patches/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(elapsed_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": args.dtype,
+        "data": "synthetic (BASELINE generator: near-white background + N(0,4), H&E-like blobs ~40%)",
+        "config": {
+            "workload": feed.workload,
+            "global_batch": args.batch * world,
+            "batch_per_gpu": args.batch,
+            "parallelism": f"slide-sharded x{world}, no data-path collective",
+            "l2": "inputs larger than L2 (slides resident in HBM, random patches; outputs stream out)",
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": feed.kernel,
+            "achieved": round(achieved, 1),
+            "peak": peak,
+            "peak_kind": peak_kind,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": traffic,
+            "algorithmic_bytes_per_patch": feed.bytes_per_patch,
+            "per_launch_ms": round(k_ms, 4),
+        },
+        "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "sampler": {"attempts": int(st.attempts), "specs": int(st.seq), "slow_evals": int(st.slow_evals)},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_15217_b200 import _native as N
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pf, plan, slides = build_slides(args, rank, world)
+    if args.config == "5":
+        run_sweep(args, pf, plan, slides, rank, world, local, torch, dist, N)
+        return
+    feed = make_feed(args, pf, plan, slides, rank)
+    elapsed_ms, stage_ms, launches, clocks = timed_run(feed, args, torch, dist, world, local, N)
+    st = feed.sampler.check()
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(pf, loader, mc, max(3, min(args.steps, 10)), torch)
+        e2e = feed.e2e_fn(pf, feed.loader, max(3, min(args.steps, 10)), torch)
         if world > 1:
             te = torch.tensor([e2e["value"]], dtype=torch.float64, device="cuda")
             dist.all_reduce(te, op=dist.ReduceOp.SUM)
@@ -282,49 +411,41 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, steps=args.cpu_steps)
     if rank == 0:
-        line = {
-            "metric": METRIC,
-            "value": round(value, 1),
-            "unit": "patches/s",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": round(elapsed_ms / args.steps, 4),
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": args.dtype,
-            "data": "synthetic (BASELINE generator: near-white background + N(0,4), H&E-like blobs ~40%)",
-            "config": {
-                "workload": ("C3: " if args.mixed_mpp else "C2: ") + f"{args.slides} slides {args.width}x{args.height} "
-                            "per GPU in HBM, sat>0.07+morph mask on 1/32 thumbnail, epoch_stream sampler 224px "
-                            "min_fg 0.40, DINOv2 multi-crop 2x224 + 8x96 " + args.dtype + " NCHW",
-                "global_batch": args.batch * world,
-                "batch_per_gpu": args.batch,
-                "parallelism": f"slide-sharded x{world}, no data-path collective",
-                "l2": "inputs larger than L2 (62 GB of slides per GPU; 1.07 GB of crops written per step)",
-            },
-            "roofline": {
-                "bound": "hbm",
-                "kernel": "multicrop_kernel (2 launches/step: global + local crop groups)",
-                "achieved": round(achieved, 1),
-                "peak": peak,
-                "peak_kind": peak_kind,
-                "unit": "GB/s",
-                "frac": round(achieved / peak, 4),
-                "traffic": traffic,
-                "algorithmic_bytes_per_patch": bpp,
-            },
-            "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
-            "sampler": {"attempts": int(st.attempts), "specs": int(st.seq), "slow_evals": int(st.slow_evals)},
-            "gpu_launches": int(launches),
-            "clocks": clocks,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-        }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(result_line(feed, args, world, elapsed_ms, stage_ms, launches, clocks, st, e2e, cpu)), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_sweep(args, pf, plan, slides, rank, world, local, torch, dist, N):
+    """BASELINE config 5: one 100000x80000 slide; patch 224/256/512 -> 224, batch 256..8192,
+    L in {0, 4, 8} local crops, fp32 vs bf16.  Every point -> profiles/sweep (JSON lines);
+    the headline line is the default point (224, 1024, L=8, bf16)."""
+    out_dir = Path(os.environ.get("PF_SWEEP_DIR", ROOT / "gpurun_out"))
+    out_dir.mkdir(parents=True, exist_ok=True)
+    points = []
+    head = None
+    for patch in (224, 256, 512):
+        for batch in (256, 1024, 4096, 8192):
+            for n_local in (0, 4, 8):
+                for dtype in ("bf16", "f32"):
+                    a = argparse.Namespace(**vars(args))
+                    a.batch, a.dtype, a.steps, a.warmup = batch, dtype, max(2, min(args.steps, 5)), 2
+                    feed = make_feed(a, pf, plan, slides, rank, n_local=n_local, patch=patch)
+                    elapsed_ms, stage_ms, launches, clocks = timed_run(feed, a, torch, dist, world, local, N)
+                    st = feed.sampler.check()
+                    line = result_line(feed, a, world, elapsed_ms, stage_ms, launches, clocks, st, None, None)
+                    line["point"] = {"patch": patch, "batch": batch, "n_local": n_local, "dtype": dtype}
+                    points.append(line)
+                    if (patch, batch, n_local, dtype) == (224, 1024, 8, "bf16"):
+                        head = line
+                    del feed
+                    torch.cuda.empty_cache()
+    if rank == 0:
+        (out_dir / "sweep_config5.jsonl").write_text("".join(json.dumps(p) + "\n" for p in points))
+        head = dict(head or points[-1])
+        head["sweep"] = [{**p["point"], "patches_per_s": p["value"], "achieved_gbs": p["roofline"]["achieved"],
+                          "frac": p["roofline"]["frac"]} for p in points]
+        print(json.dumps(head), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -335,13 +456,15 @@ def cpu_baseline(args, steps=2):
     from oracle import cpu_pipeline as cp
 
     cores = cp.cpu_count()
-    per_step, cands = cp.run(cores, args.slides, args.width, args.height, candidates_per_step=1, steps=steps + 1)
+    per_step, cands = cp.run(cores, args.slides, args.width, args.height, candidates_per_step=1, steps=steps + 1,
+                             augment=args.config != "1")
     timed = per_step[1:]
     t = sum(d for d, _ in timed)
     n = sum(m for _, m in timed)
     return {"value": round(n / t, 4) if t > 0 else 0.0, "unit": "patches/s", "cores": cores, "kind": "port",
-            "sample": f"{steps} steps x {cores} workers x 1 epoch_stream candidate each (+ read_region + torchvision "
-                      f"multi-crop of accepted specs); {n} patches in {t:.1f} s; {cands} candidates total"}
+            "sample": f"{steps} steps x {cores} workers x 1 epoch_stream candidate each (+ read_region + "
+                      f"{'torchvision multi-crop' if args.config != '1' else 'normalize_patch'} of accepted specs); "
+                      f"{n} patches in {t:.1f} s; {cands} candidates total"}
 
 
 def run_reference(args):
@@ -352,7 +475,7 @@ def run_reference(args):
 
     cores = cp.cpu_count()
     per_step, cands = cp.run(cores, args.slides, args.width, args.height, candidates_per_step=1,
-                             steps=args.warmup + args.steps)
+                             steps=args.warmup + args.steps, augment=args.config != "1")
     timed = per_step[args.warmup:]
     t = sum(d for d, _ in timed)
     n = sum(m for _, m in timed)
@@ -371,8 +494,10 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": args.dtype,
         "data": "synthetic (numpy restatement of the same generator, tiles rendered on first touch)",
-        "config": {"workload": f"C2 on CPU: {args.slides} slides {args.width}x{args.height}, reference epoch_stream "
-                               "(numpy even-odd overlap), read_region, torchvision multi-crop 2x224+8x96, bf16",
+        "config": {"workload": f"C{args.config} on CPU: {args.slides} slides {args.width}x{args.height}, reference "
+                               "epoch_stream (numpy even-odd overlap), read_region, " +
+                               ("normalize_patch (ImageNet) fp32" if args.config == "1" else
+                                "torchvision multi-crop 2x224+8x96, bf16"),
                    "global_batch": args.batch, "parallelism": f"{cores} worker processes, seed + worker"},
         "cpu_baseline": {"value": round(value, 4), "unit": "patches/s", "cores": cores, "kind": "port",
                          "sample": f"{len(timed)} steps x {cores} workers x 1 sampler candidate; {n} patches, "

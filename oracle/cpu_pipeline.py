@@ -189,7 +189,7 @@ def augment_patch(src, rs, mean, std):
 
 def _worker_main(args):
     """Process worker: build its slides, then run `candidates` sampler attempts + read + augment per step."""
-    (wid, seed, n_slides, width, height, candidates, steps, mean, std, q, polys) = args
+    (wid, seed, n_slides, width, height, candidates, steps, mean, std, q, polys, augment) = args
     import torch
 
     torch.set_num_threads(1)
@@ -205,7 +205,11 @@ def _worker_main(args):
             spec = w.candidate()
             if spec is not None:
                 si, x, y = spec
-                augment_patch(slides[si].read_region224(x, y), rs, mean, std)
+                px = slides[si].read_region224(x, y)
+                if augment:
+                    augment_patch(px, rs, mean, std)
+                else:  # config 1: normalize_patch with ImageNet mean/std, NCHW fp32
+                    np.ascontiguousarray(port.normalize_patch(px, mean, std).transpose(2, 0, 1))
                 made += 1
         q.put(("step", wid, step, time.perf_counter() - t0, made))
     q.put(("done", wid, 0, 0.0, w.candidates))
@@ -217,7 +221,7 @@ def _slide_polygon(a):
 
 
 def run(n_workers, n_slides, width, height, candidates_per_step, steps, seed=0, mean=(0.485, 0.456, 0.406),
-        std=(0.229, 0.224, 0.225)):
+        std=(0.229, 0.224, 0.225), augment=True):
     """Yields per-step (wall_seconds, patches) aggregated over the worker pool."""
     import multiprocessing as mp
 
@@ -226,7 +230,7 @@ def run(n_workers, n_slides, width, height, candidates_per_step, steps, seed=0, 
         polys = pool.map(_slide_polygon, [(width, height, 1000 + i) for i in range(n_slides)])
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker_main, args=((i, seed, n_slides, width, height, candidates_per_step, steps, mean,
-                                                    std, q, polys),)) for i in range(n_workers)]
+                                                    std, q, polys, augment),)) for i in range(n_workers)]
     for p in procs:
         p.start()
     ready = 0

@@ -179,3 +179,72 @@ def read_patch_pack(path) -> np.ndarray:
     if len(payload) != count * size * size * 3 * dt.itemsize:
         raise PackFormatError(f"payload is {len(payload)} bytes, header implies {count * size * size * 3 * dt.itemsize}")
     return np.frombuffer(payload, dtype=dt.newbyteorder("<")).reshape(count, size, size, 3).astype(dt)
+
+
+class RegionLoader:
+    """Sampler -> read_region -> normalise, on device (BASELINE config 1, no augmentation).
+
+    ``slides``: list of (GpuSlide, ForegroundPolygon).  Each ``next_batch`` returns a
+    [batch, 3, S, S] tensor of (v/255 - mean)/std (``dtype`` f32/bf16) or raw uint8, for the
+    next ``batch`` specs of the reference epoch_stream.  The sampler for step k+1 runs on a
+    side stream while step k is read (``prefetch``).
+    """
+
+    def __init__(self, slides, sampler_config, *, batch_size: int = 256, dtype: str = "f32", layout: str = "nchw",
+                 mean=IMAGENET_MEAN, std=IMAGENET_STD, prefetch: bool = True, window=None, rounds: int = 4):
+        torch = N.require_cuda()
+        from .sampler import GpuSampler
+
+        self.slide_set = SlideSet([s for s, _ in slides])
+        self.sampler = GpuSampler(sampler_config, slides, slide_set=self.slide_set, window=window, rounds=rounds)
+        self.batch_size = batch_size
+        self.out_size = sampler_config.patch_size
+        self.dtype, self.layout, self.mean, self.std = dtype, layout, mean, std
+        self.prefetch = prefetch
+        self.specs_slots = [torch.empty((batch_size, 64), dtype=torch.uint8, device="cuda") for _ in range(2)]
+        self._side = torch.cuda.Stream()
+        self._ready = [None, None]
+        self._free = [torch.cuda.Event(), torch.cuda.Event()]
+        self._next = 0
+        S = self.out_size
+        tdt = {"u8": torch.uint8, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+        shape = (batch_size, 3, S, S) if layout == "nchw" else (batch_size, S, S, 3)
+        self.out = torch.empty(shape, dtype=tdt, device="cuda")
+
+    def next_batch(self, stream=None, marks: list | None = None):
+        torch = N.require_cuda()
+        st = stream or torch.cuda.current_stream()
+
+        def mark(name):
+            if marks is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(st)
+                marks.append((name, ev))
+
+        n = self.batch_size
+        mark("begin")
+        if not self.prefetch:
+            cur = 0
+            self.sampler.next_batch(n, out=self.specs_slots[0], stream=st)
+            mark("sample")
+        else:
+            cur = self._next
+            if self._ready[cur] is None:
+                self._side.wait_stream(st)
+                self.sampler.next_batch(n, out=self.specs_slots[cur], stream=self._side)
+                self._ready[cur] = torch.cuda.Event()
+                self._ready[cur].record(self._side)
+            st.wait_event(self._ready[cur])
+            mark("sample_wait")
+            nxt = 1 - cur
+            self._side.wait_event(self._free[nxt])
+            self.sampler.next_batch(n, out=self.specs_slots[nxt], stream=self._side)
+            self._ready[nxt] = torch.cuda.Event()
+            self._ready[nxt].record(self._side)
+            self._next = nxt
+        self.slide_set.read_regions(self.specs_slots[cur], self.out_size, dtype=self.dtype, layout=self.layout,
+                                    mean=self.mean, std=self.std, out=self.out, stream=st, planned=True)
+        mark("read")
+        if self.prefetch:
+            self._free[cur].record(st)
+        return {"patches": self.out, "specs": self.specs_slots[cur]}
