@@ -140,92 +140,211 @@ __device__ __forceinline__ void write_out(void* out, int layout, int n_idx, int 
     }
 }
 
-// One CTA per spec.  Passthrough copies the clamped window; otherwise the
-// PIL two-pass resample runs in bands of output rows with a uint8
-// intermediate in shared memory.
+// read_region on device.  Grid: (spec, band of kRRBand output rows).
+//  * passthrough (side == out): the band's source rows are staged from the
+//    tile pyramid with 16-byte cp.async (whole tile rows; clamped per-pixel
+//    gather only when the window touches the level edge), then written with
+//    the normalising epilogue (3x256 LUT) as 16-byte NCHW rows or HWC words;
+//  * resample (side != out): the band-0 CTA of the spec runs the PIL two-pass
+//    fixed-point resample for the whole patch (coefficients built in shared
+//    memory, source rows staged per band, horizontal pass into planar uint8,
+//    vertical pass straight into the epilogue); the other band CTAs exit.
 constexpr int kRRThreads = 256;
-constexpr int kRRInterBytes = 48 * 1024;
+constexpr int kRRBand = 32;
+constexpr int kRRSmem = 96 * 1024;
+
+__device__ __forceinline__ void rr_cp_async16(void* smem_dst, const void* gmem_src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src));
+}
+__device__ __forceinline__ void rr_cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Stage level rows Y0+r, r in [0, nr), columns [X0, X0+w) into stg (row stride row_bytes);
+// returns the byte offset of column X0 inside a staged row.
+__device__ int stage_level_rows(const pf_slide_desc& sd, int L, int X0, int Y0, int w, int nr, uint8_t* stg,
+                                int row_bytes, bool fast) {
+    const int T = sd.tile_size;
+    const int LW = sd.width[L], LH = sd.height[L];
+    const uint8_t* lvl = reinterpret_cast<const uint8_t*>(sd.level_ptr[L]);
+    if (fast) {
+        const int tx0 = X0 / T, ntx = (X0 + w - 1) / T - tx0 + 1;
+        const int cpr = T * 3 / 16;
+        const size_t tile_bytes = (size_t)T * T * 3;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int rr = warp; rr < nr; rr += blockDim.x / 32) {
+            const int Y = Y0 + rr;
+            const int ty = Y / T, v = Y - ty * T;
+            const uint8_t* grow = lvl + ((size_t)ty * sd.tiles_x[L] + tx0) * tile_bytes + (size_t)v * T * 3;
+            uint8_t* srow = stg + rr * row_bytes;
+            for (int t = 0; t < ntx; ++t)
+                for (int ch = lane; ch < cpr; ch += 32) rr_cp_async16(srow + t * T * 3 + ch * 16, grow + t * tile_bytes + ch * 16);
+        }
+        rr_cp_async_wait_all();
+        return (X0 - tx0 * T) * 3;
+    }
+    for (int q = threadIdx.x; q < nr * w; q += blockDim.x) {
+        const int rr = q / w, xx = q - rr * w;
+        const uint8_t* s = level_pixel(sd, L, clampi(X0 + xx, 0, LW - 1), clampi(Y0 + rr, 0, LH - 1));
+        uint8_t* d = stg + rr * row_bytes + xx * 3;
+        d[0] = s[0];
+        d[1] = s[1];
+        d[2] = s[2];
+    }
+    return 0;
+}
+
+template <int kDtype>
+struct RROut;
+template <>
+struct RROut<PF_U8> {
+    using T = uint8_t;
+};
+template <>
+struct RROut<PF_F32> {
+    using T = float;
+};
+template <>
+struct RROut<PF_BF16> {
+    using T = __nv_bfloat16;
+};
 
 template <int kDtype>
 __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide_desc* slides,
-                                                                  const pf_patch_spec* specs,
-                                                                  int out_size, int layout,
-                                                                  NormParams np, void* out) {
+                                                                  const pf_patch_spec* specs, int S, int layout,
+                                                                  int n_bands, NormParams np, void* out_v) {
+    using OT = typename RROut<kDtype>::T;
     extern __shared__ __align__(16) uint8_t smem[];
-    const pf_patch_spec sp = specs[blockIdx.x];
-    const pf_slide_desc& s = slides[sp.slide];
-    const int L = sp.level;
-    const int W = s.width[L], H = s.height[L];
-    const int side = sp.side, S = out_size;
+    const int spec_i = blockIdx.x / n_bands, band = blockIdx.x - spec_i * n_bands;
+    const pf_patch_spec sp = specs[spec_i];
     const bool skip_pass = layout & PF_SKIP_PASSTHROUGH;
-    layout &= 0xff;
+    const int lay = layout & 0xff;
+    const pf_slide_desc& sd = slides[sp.slide];
+    const int L = sp.level;
+    const int LW = sd.width[L], LH = sd.height[L];
+    const int side = sp.side;
+    const bool pass = side == S;
+    if (pass && skip_pass) return;
+    if (!pass && band > 0) return;
+    OT* out = reinterpret_cast<OT*>(out_v);
+    // LUT for the epilogue
+    OT* lut = reinterpret_cast<OT*>(smem);
+    uint8_t* work = smem + ((3 * 256 * sizeof(OT) + 15) & ~size_t(15));
+    const int work_bytes = kRRSmem - (int)(work - smem);
+    for (int i = threadIdx.x; i < 3 * 256; i += kRRThreads) {
+        const int c = i >> 8;
+        const uint8_t v = (uint8_t)(i & 255);
+        if constexpr (kDtype == PF_U8) lut[i] = v;
+        else {
+            const float f = __fdiv_rn(__fdiv_rn((float)v, 255.0f) - np.mean[c], np.stdv[c]);
+            if constexpr (kDtype == PF_F32) lut[i] = f;
+            else lut[i] = __float2bfloat16_rn(f);
+        }
+    }
+    const size_t plane = (size_t)S * S;
+    OT* o = out + (size_t)spec_i * 3 * plane;
+    const int T = sd.tile_size;
 
-    if (side == S) {
-        if (skip_pass) return;
-        for (int p = threadIdx.x; p < S * S; p += blockDim.x) {
-            const int y = p / S, x = p - y * S;
-            const int X = clampi(sp.sx + x, 0, W - 1), Y = clampi(sp.sy + y, 0, H - 1);
-            const uint8_t* src = level_pixel(s, L, X, Y);
-            const uint8_t rgb[3] = {src[0], src[1], src[2]};
-            write_out<kDtype>(out, layout, blockIdx.x, S, y, x, rgb, np);
+    if (pass) {
+        const int y0 = band * kRRBand, y1 = min(S, y0 + kRRBand);
+        if (y0 >= S) return;
+        const int nr = y1 - y0;
+        const int X0 = sp.sx, Y0 = sp.sy + y0;
+        const bool fast = X0 >= 0 && Y0 >= 0 && X0 + S <= LW && Y0 + nr <= LH && (T % 16) == 0;
+        const int row_bytes = fast ? ((X0 + S - 1) / T - X0 / T + 1) * T * 3 : ((S * 3 + 15) & ~15);
+        const int base = stage_level_rows(sd, L, X0, Y0, S, nr, work, row_bytes, fast);
+        __syncthreads();
+        if (lay == PF_NCHW && (S % 4) == 0) {
+            const int G = S / 4;
+            for (int q = threadIdx.x; q < 3 * nr * G; q += kRRThreads) {
+                const int c = q / (nr * G);
+                const int rem = q - c * nr * G;
+                const int rr = rem / G, x0 = (rem - rr * G) * 4;
+                const uint8_t* s = work + rr * row_bytes + base + x0 * 3 + c;
+                OT v[4] = {lut[c * 256 + s[0]], lut[c * 256 + s[3]], lut[c * 256 + s[6]], lut[c * 256 + s[9]]};
+                OT* dst = o + c * plane + (size_t)(y0 + rr) * S + x0;
+                if constexpr (sizeof(OT) == 4) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+                else if constexpr (sizeof(OT) == 2) *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(v);
+                else *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(v);
+            }
+        } else if (lay == PF_HWC && kDtype == PF_U8 && (S * 3) % 4 == 0) {
+            const int W4 = S * 3 / 4;
+            for (int q = threadIdx.x; q < nr * W4; q += kRRThreads) {
+                const int rr = q / W4, b0 = (q - rr * W4) * 4;
+                const uint8_t* s = work + rr * row_bytes + base + b0;
+                const uint32_t w = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16) | ((uint32_t)s[3] << 24);
+                *reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(o) + (size_t)(y0 + rr) * S * 3 + b0) = w;
+            }
+        } else {
+            for (int q = threadIdx.x; q < nr * S; q += kRRThreads) {
+                const int rr = q / S, x = q - rr * S;
+                const uint8_t* s = work + rr * row_bytes + base + x * 3;
+                for (int c = 0; c < 3; ++c) {
+                    const size_t idx = lay == PF_HWC ? ((size_t)(y0 + rr) * S + x) * 3 + c : c * plane + (size_t)(y0 + rr) * S + x;
+                    o[idx] = lut[c * 256 + s[c]];
+                }
+            }
         }
         return;
     }
 
-    // coefficient table (square window: one table serves both axes)
+    // ---- PIL resample of the whole window (one CTA per spec)
     const AxisPlan ap = axis_plan(side, S);
-    int* s_xmin = reinterpret_cast<int*>(smem);
+    const int K = ap.ksize;
+    int* s_xmin = reinterpret_cast<int*>(work);
     int* s_xsize = s_xmin + S;
     int32_t* s_w = s_xsize + S;
-    double* s_red = reinterpret_cast<double*>(smem + (((size_t)(2 * S + S * ap.ksize) * 4 + 15) & ~size_t(15)));
-    uint8_t* s_inter = reinterpret_cast<uint8_t*>(s_red + 2);
+    double* s_red = reinterpret_cast<double*>(work + (((size_t)(2 * S + S * K) * 4 + 15) & ~size_t(15)));
+    uint8_t* buf = reinterpret_cast<uint8_t*>(s_red + 2);
+    const int buf_bytes = work_bytes - (int)(buf - work);
     build_axis_table(side, S, RS_PIL, s_xmin, s_xsize, s_w, s_red);
-    const int K = ap.ksize;
-    const int row_bytes = S * 3;
-    const int max_rows = kRRInterBytes / row_bytes;
-
+    const int sx = sp.sx, sy = sp.sy;
+    const bool fast_all = sx >= 0 && sy >= 0 && sx + side <= LW && sy + side <= LH && (T % 16) == 0;
+    const int row_bytes = fast_all ? ((sx + side - 1) / T - sx / T + 1) * T * 3 : ((side * 3 + 15) & ~15);
+    const int max_rows = buf_bytes / (row_bytes + 3 * S);
     int y0 = 0;
     while (y0 < S) {
-        // grow the band while its source rows fit the intermediate buffer
         const int r0 = s_xmin[y0];
         int y1 = y0 + 1;
         while (y1 < S && s_xmin[y1] + s_xsize[y1] - r0 <= max_rows) ++y1;
         const int r1 = s_xmin[y1 - 1] + s_xsize[y1 - 1];
-        // horizontal pass: source rows [r0, r1) -> s_inter
-        for (int p = threadIdx.x; p < (r1 - r0) * S; p += blockDim.x) {
-            const int rr = p / S, x = p - rr * S;
-            const int Y = clampi(sp.sy + r0 + rr, 0, H - 1);
+        const int nr = r1 - r0;
+        uint8_t* stg = buf;
+        uint8_t* hb = buf + nr * row_bytes;  // [3][nr][S]
+        const int base = stage_level_rows(sd, L, sx, sy + r0, side, nr, stg, row_bytes, fast_all);
+        __syncthreads();
+        for (int q = threadIdx.x; q < nr * S; q += kRRThreads) {
+            const int rr = q / S, x = q - rr * S;
+            const uint8_t* srow = stg + rr * row_bytes + base;
             const int xmin = s_xmin[x], xs = s_xsize[x];
             int32_t a0 = 1 << 21, a1 = 1 << 21, a2 = 1 << 21;
             for (int k = 0; k < xs; ++k) {
-                const int X = clampi(sp.sx + xmin + k, 0, W - 1);
-                const uint8_t* src = level_pixel(s, L, X, Y);
+                const uint8_t* p = srow + (xmin + k) * 3;
                 const int32_t wk = s_w[x * K + k];
-                a0 += (int32_t)src[0] * wk;
-                a1 += (int32_t)src[1] * wk;
-                a2 += (int32_t)src[2] * wk;
+                a0 += (int32_t)p[0] * wk;
+                a1 += (int32_t)p[1] * wk;
+                a2 += (int32_t)p[2] * wk;
             }
-            uint8_t* d = s_inter + (size_t)rr * row_bytes + x * 3;
-            d[0] = clip_shift(a0, 22);
-            d[1] = clip_shift(a1, 22);
-            d[2] = clip_shift(a2, 22);
+            hb[rr * S + x] = clip_shift(a0, 22);
+            hb[(nr + rr) * S + x] = clip_shift(a1, 22);
+            hb[(2 * nr + rr) * S + x] = clip_shift(a2, 22);
         }
         __syncthreads();
-        // vertical pass: output rows [y0, y1)
-        for (int p = threadIdx.x; p < (y1 - y0) * S; p += blockDim.x) {
-            const int yy = p / S, x = p - yy * S;
+        for (int q = threadIdx.x; q < (y1 - y0) * S; q += kRRThreads) {
+            const int yy = q / S, x = q - yy * S;
             const int y = y0 + yy;
             const int ymin = s_xmin[y] - r0, ys = s_xsize[y];
-            int32_t a0 = 1 << 21, a1 = 1 << 21, a2 = 1 << 21;
+            int32_t a[3] = {1 << 21, 1 << 21, 1 << 21};
             for (int k = 0; k < ys; ++k) {
-                const uint8_t* src = s_inter + (size_t)(ymin + k) * row_bytes + x * 3;
                 const int32_t wk = s_w[y * K + k];
-                a0 += (int32_t)src[0] * wk;
-                a1 += (int32_t)src[1] * wk;
-                a2 += (int32_t)src[2] * wk;
+                const int b = (ymin + k) * S + x;
+                a[0] += (int32_t)hb[b] * wk;
+                a[1] += (int32_t)hb[nr * S + b] * wk;
+                a[2] += (int32_t)hb[2 * nr * S + b] * wk;
             }
-            const uint8_t rgb[3] = {clip_shift(a0, 22), clip_shift(a1, 22), clip_shift(a2, 22)};
-            write_out<kDtype>(out, layout, blockIdx.x, S, y, x, rgb, np);
+            for (int c = 0; c < 3; ++c) {
+                const size_t idx = lay == PF_HWC ? ((size_t)y * S + x) * 3 + c : c * plane + (size_t)y * S + x;
+                o[idx] = lut[c * 256 + clip_shift(a[c], 22)];
+            }
         }
         __syncthreads();
         y0 = y1;
@@ -243,6 +362,7 @@ __global__ void normalize_kernel(const uint8_t* in, int64_t n, NormParams np, vo
 }  // namespace pf
 
 using namespace pf;
+
 
 extern "C" int pf_normalize(const uint8_t* in_hwc, int64_t n_pixels, int32_t dtype, const float* mean3,
                             const float* std3, void* out, void* stream) {
@@ -308,7 +428,7 @@ extern "C" int pf_plan_regions(const pf_slide_desc* slides_dev, pf_patch_spec* s
 extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_spec* specs_dev,
                                int32_t n, int32_t out_size, int32_t dtype, int32_t layout,
                                const float* mean3, const float* std3, void* out, void* stream) {
-    if (n < 0 || out_size < 1 || out_size > 4096 || (n > 0 && (!slides_dev || !specs_dev || !out)))
+    if (n < 0 || out_size < 1 || (n > 0 && (!slides_dev || !specs_dev || !out)))
         return fail(PF_ERR_INVALID_ARG, "pf_read_regions: bad arguments");
     if ((layout & 0xff) != PF_HWC && (layout & 0xff) != PF_NCHW)
         return fail(PF_ERR_INVALID_ARG, "pf_read_regions: bad layout");
@@ -320,35 +440,24 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
         np.mean[c] = mean3 ? mean3[c] : 0.5f;
         np.stdv[c] = std3 ? std3[c] : 0.5f;
     }
-    // worst-case ksize for down-ratios up to 15x
-    const int ksize_max = 32;
-    const size_t smem = ((size_t)(2 * out_size + out_size * ksize_max) * 4 + 15) / 16 * 16 + 16 + kRRInterBytes;
+    const int n_bands = (out_size + kRRBand - 1) / kRRBand;
+    const long long grid = (long long)n * n_bands;
     cudaStream_t st = as_stream(stream);
     int rc;
+#define PF_RR_LAUNCH(DT)                                                                                          \
+    rc = check_cuda(cudaFuncSetAttribute(read_regions_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                         kRRSmem),                                                                \
+                    "cudaFuncSetAttribute");                                                                      \
+    if (rc) return rc;                                                                                            \
+    read_regions_kernel<DT><<<(unsigned)grid, kRRThreads, kRRSmem, st>>>(slides_dev, specs_dev, out_size, layout,  \
+                                                                          n_bands, np, out);
     switch (dtype) {
-        case PF_U8:
-            rc = check_cuda(cudaFuncSetAttribute(read_regions_kernel<PF_U8>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                            "cudaFuncSetAttribute");
-            if (rc) return rc;
-            read_regions_kernel<PF_U8><<<n, kRRThreads, smem, st>>>(slides_dev, specs_dev, out_size, layout, np, out);
-            break;
-        case PF_F32:
-            rc = check_cuda(cudaFuncSetAttribute(read_regions_kernel<PF_F32>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                            "cudaFuncSetAttribute");
-            if (rc) return rc;
-            read_regions_kernel<PF_F32><<<n, kRRThreads, smem, st>>>(slides_dev, specs_dev, out_size, layout, np, out);
-            break;
-        case PF_BF16:
-            rc = check_cuda(cudaFuncSetAttribute(read_regions_kernel<PF_BF16>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                            "cudaFuncSetAttribute");
-            if (rc) return rc;
-            read_regions_kernel<PF_BF16><<<n, kRRThreads, smem, st>>>(slides_dev, specs_dev, out_size, layout, np, out);
-            break;
-        default:
-            return fail(PF_ERR_INVALID_ARG, "pf_read_regions: bad dtype");
+        case PF_U8: PF_RR_LAUNCH(PF_U8) break;
+        case PF_F32: PF_RR_LAUNCH(PF_F32) break;
+        case PF_BF16: PF_RR_LAUNCH(PF_BF16) break;
+        default: return fail(PF_ERR_INVALID_ARG, "pf_read_regions: bad dtype");
     }
+#undef PF_RR_LAUNCH
     return after_launch("read_regions_kernel");
 }
+
