@@ -142,3 +142,31 @@ def test_loader_end_to_end(pf):
     b2 = ref.next_batch()
     assert torch.equal(b2["specs"], out2["specs"]) and torch.equal(b2["global_crops"], out2["global_crops"])
     assert bool(out2["global_crops"].float().abs().sum() > 0)
+
+
+def test_hue_every_colour_exact(pf):
+    """Every one of the 2^24 RGB colours through the kernel's adjust_hue (random shift in
+    [-0.5, 0.5] per crop, the other jitter factors pinned to 1, identity crop): bit-exact
+    against the float32 restatement (pinned to torchvision by test_aug_semantics)."""
+    torch = pytest.importorskip("torch")
+    gx, gy = 19, 18  # 342 patches of 224^2 >= 2^24 pixels
+    n = gx * gy
+    idx = (np.arange(n * 224 * 224, dtype=np.int64) % (1 << 24)).reshape(gy, gx, 224, 224)
+    rgb = np.stack([(idx >> 16) & 255, (idx >> 8) & 255, idx & 255], -1).astype(np.uint8)
+    img = np.ascontiguousarray(rgb.transpose(0, 2, 1, 3, 4).reshape(gy * 224, gx * 224, 3))
+    s = pf.GpuSlide.from_array(img, "hue", 0.25, tile_size=256, downsample_factor=4)
+    ss = pf.SlideSet([s])
+    reqs = [(0, (224 * (k % gx), 224 * (k // gx), 224, 224), 0.25, 224) for k in range(n)]
+    specs = pf.store.plan_specs(reqs, ss.records)
+    cfg = pf.mc.MultiCropConfig(n_global=1, n_local=0, global_scale=(1.0, 1.0), ratio=(1.0, 1.0), p_flip=0.0,
+                                p_jitter=1.0, p_gray=0.0, brightness=0.0, contrast=0.0, saturation=0.0, hue=0.5,
+                                p_blur=[0.0], p_solarize=[0.0])
+    g, _, prm = _run(pf, ss, specs, cfg, "u8", seed=7)
+    g = g.cpu().numpy()
+    for k in range(n):
+        p = prm[k, 0]
+        assert p["height"] == 224 and p["width"] == 224 and p["brightness"] == 1.0
+        src = rgb[k // gx, k % gx]
+        want = A.hue(src, float(p["hue"]))
+        got = g[0, k].transpose(1, 2, 0)
+        assert np.array_equal(got, want), (k, float(p["hue"]), int((got != want).any(-1).sum()))
