@@ -14,6 +14,12 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 
 
+# one-off setup kernels (slide rendering, pyramid, thumbnail, mask, polygon index, RRC tables):
+# excluded so the shares are those of the timed step
+SETUP = ("synth_level0", "box_downsample", "box32_warp", "mask_kernel", "morph_kernel", "rrc_table_kernel",
+         "poly_index", "thumbnail", "field_kernel")
+
+
 def launches(path):
     rows = list(csv.reader(open(path)))
     hdr = None
@@ -27,6 +33,8 @@ def launches(path):
             d = dict(zip(hdr, r))
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 k = d["Kernel Name"].split("(")[0].replace("void ", "")
+                if any(t in k for t in SETUP):
+                    continue
                 v = float(d["Metric Value"].replace(",", ""))
                 scale = {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(d["Metric Unit"], 1e-3)
                 per[k] += v * scale
