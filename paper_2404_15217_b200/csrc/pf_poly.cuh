@@ -155,6 +155,44 @@ __device__ inline int warp_overlap_count(const PolyView& P, double x, double y, 
     const int lane = threadIdx.x & 31;
     const int nw = overlap_words(grid);
     const double sx = __ddiv_rn(w, (double)grid), sy = __ddiv_rn(h, (double)grid);
+    // Exact shortcut for windows no edge comes near: every lattice row lies in one of the slabs
+    // ka..kb and every lattice point in [x, x_last].  If no slab has an edge whose x-bounds
+    // overlap [x, x_last] (row_mask would evaluate no x_at), each row's mask is all-ones or
+    // all-zeros by its slab's parity (e1 - i_hi) & 1 -- row_mask's own i_lo/i_hi collapse to the
+    // window's -- so when every parity agrees the count is grid^2 or 0.
+    if (P.n_y >= 2) {
+        const double ylast = lattice(y, sy, grid, false), xlast = lattice(x, sx, grid, false);
+        const double Yfirst = __ldg(P.Y), Ylast = __ldg(P.Y + P.n_y - 1);
+        const bool rows_outside = !(y >= Yfirst) || !(ylast < Ylast);  // some rows get an empty mask
+        const int ka = y >= Yfirst ? slab_of(P, y) : 0;
+        const int kb = ylast < Ylast ? slab_of(P, ylast) : P.n_y - 2;
+        bool amb = ka < 0;
+        int par_or = 0, par_and = 1;
+        for (int k = ka + lane; !amb && k <= kb; k += 32) {
+            const int e0 = __ldg(P.slab_off + k), e1 = __ldg(P.slab_off + k + 1);
+            int a = e0, b = e1;
+            while (a < b) {
+                const int m = (a + b) >> 1;
+                if (__ldg(P.hi + m) < x) a = m + 1;
+                else b = m;
+            }
+            const int i_lo = a;
+            b = e1;
+            while (a < b) {
+                const int m = (a + b) >> 1;
+                if (__ldg(P.lo + m) > xlast) b = m;
+                else a = m + 1;
+            }
+            amb |= i_lo < a;
+            const int par = (e1 - a) & 1;
+            par_or |= par;
+            par_and &= par;
+        }
+        amb = __any_sync(0xffffffffu, amb);
+        par_or = __any_sync(0xffffffffu, par_or);
+        par_and = __all_sync(0xffffffffu, par_and);
+        if (!amb && (par_or == 0 || (par_and && !rows_outside))) return par_or ? grid * grid : 0;
+    }
     uint32_t* corner = smem;                      // (grid+1) rows
     uint32_t* centre = smem + (grid + 1) * nw;    // grid rows
     const int n_rows = 2 * grid + 1;

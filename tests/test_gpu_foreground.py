@@ -71,3 +71,30 @@ def test_polygon_from_device_mask_pipeline(pf, goldens, golden_arrays):
     poly = pf.polygon_from_mask(m, slide_id="blob")
     for a, b in zip(poly.rings, goldens["blob_poly"]["rings"]):
         assert np.array_equal(a, np.asarray(b))
+
+
+def test_overlap_uniform_window_shortcut_vs_oracle(pf, goldens):
+    """Windows deep inside / outside / straddling horizontal and vertical edges, on polygons with
+    holes and axis-aligned edges: the device's whole-window shortcut (no edge near the lattice)
+    must equal the row-by-row even-odd count of the reference."""
+    rs = np.random.default_rng(21)
+    ring = lambda x0, y0, x1, y1: np.array([[x0, y0], [x1, y0], [x1, y1], [x0, y1]], float)
+    polys = [
+        pf.rect_polygon(100, 100, 400, 300),
+        pf.ForegroundPolygon([ring(0, 0, 600, 600), ring(200, 200, 400, 400)[::-1]]),  # hole
+        pf.ForegroundPolygon.from_json_dict(goldens["blob_poly"]),
+    ]
+    for poly in polys:
+        bx0, by0, bx1, by1 = poly.bounding_box()
+        n = 120
+        w = rs.choice([16.0, 64.0, 100.0, 224.0], size=n)
+        x = rs.uniform(bx0 - 120, bx1 + 20, n)
+        y = rs.uniform(by0 - 120, by1 + 20, n)
+        k = rs.random(n) < 0.4  # snap onto the 100-px lattice: windows touching edges exactly
+        x[k], y[k] = np.round(x[k] / 100) * 100, np.round(y[k] / 100) * 100
+        rects = np.stack([x, y, w, w], 1)
+        for grid in (128, 64):
+            got = pf.overlap_fractions(poly, rects, grid=grid).cpu().numpy()
+            want = [port.overlap_fraction(poly.rings, tuple(r), grid) for r in rects]
+            assert got.tolist() == want, grid
+            assert 0.0 < np.mean(np.asarray(want) == 1.0) < 1.0  # both shortcut outcomes exercised
