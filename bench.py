@@ -25,6 +25,8 @@ import subprocess
 import sys
 import threading
 import time
+
+import numpy as np
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
@@ -39,8 +41,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="2", choices=["1", "2", "3", "5"],
-                    help="BASELINE config: 1 normalise-only, 2 multi-crop (default), 3 mixed mpp, 5 sweep")
+    ap.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5"],
+                    help="BASELINE config: 1 normalise-only, 2 multi-crop (default), 3 mixed mpp, "
+                         "4 whole-box slide set (tile residency), 5 sweep")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--slides", type=int, default=None)
     ap.add_argument("--width", type=int, default=None)
@@ -66,6 +69,8 @@ CONFIGS = {
     "1": dict(batch=256, slides=1, width=8192, height=8192, dtype="f32"),
     "2": dict(batch=1024, slides=16, width=40000, height=30000, dtype="bf16"),
     "3": dict(batch=2048, slides=16, width=40000, height=30000, dtype="bf16"),
+    # 128 slides, W ~ U[40000, 100000], H ~ U[30000, 80000] from a seed, 16 per GPU (sizes below unused)
+    "4": dict(batch=1024, slides=16, width=0, height=0, dtype="bf16"),
     "5": dict(batch=1024, slides=1, width=100000, height=80000, dtype="bf16"),
 }
 
@@ -151,13 +156,40 @@ def build_slides(args, rank, world):
 
     plan = rank_plan(rank, world, args.slides * world, seed=0)  # rank r owns slides [16r, 16r+16)
     slides = []
+    resident, dense = 0, 0
+    if args.config == "4":  # 128 slide sizes from one seed; rank r renders slides [16r, 16r + 16)
+        rs = np.random.default_rng(4)
+        dims = list(zip(rs.integers(40000, 100001, 128), rs.integers(30000, 80001, 128)))
     for gi in plan.slide_indices:
         sid = f"s{gi}"
-        s = synthetic_slide(sid, args.width, args.height, seed=1000 + gi, downsample_factor=4)
-        thumb, scale = s.thumbnail_device(32)
-        mask = pf.foreground.mask_device(thumb, 1, 0.07, 1)  # BASELINE: saturation > 0.07 + morphology
-        bm = pf.BinaryMask(mask.cpu().numpy().astype(bool), scale)
-        slides.append((s, pf.polygon_from_mask(bm, slide_id=sid)))
+        w, h = (int(dims[gi % 128][0]), int(dims[gi % 128][1])) if args.config == "4" else (args.width, args.height)
+        for k in range(8):
+            s = synthetic_slide(sid, w, h, seed=1000 + gi + 100_000 * k, downsample_factor=4)
+            thumb, scale = s.thumbnail_device(32)
+            mask = pf.foreground.mask_device(thumb, 1, 0.07, 1)  # BASELINE: saturation > 0.07 + morphology
+            bm = pf.BinaryMask(mask.cpu().numpy().astype(bool), scale)
+            try:
+                poly = pf.polygon_from_mask(bm, slide_id=sid)
+                break
+            except ValueError as e:
+                # the reference's ring orientation (vertex-mean probe, pkg/foreground.py:206-216) can
+                # leave a non-convex layout with negative total area; redraw that slide's tissue
+                print(f"[rank {rank}] {sid}: {e}; redrawing tissue (seed +{100_000 * (k + 1)})", file=sys.stderr)
+                del s
+        slides.append((s, poly))
+        if args.config == "4":  # keep only the tiles an admissible window can reach
+            from paper_2404_15217_b200 import residency as R
+
+            tiles = R.reachable_tiles(s.record, bm.bits, scale, R.max_footprint(s.record, 224, [(0.25, 1.0)]))
+            dense += R.dense_bytes(s.record)
+            resident += R.resident_bytes(s.record, tiles)
+            print(f"[rank {rank}] {sid} {w}x{h}: mask {bm.bits.mean():.3f}, pyramid {R.dense_bytes(s.record) / 1e9:.1f} GB"
+                  f" -> {R.resident_bytes(s.record, tiles) / 1e9:.1f} GB resident", file=sys.stderr)
+            s.compact(tiles)
+            import torch
+
+            torch.cuda.empty_cache()
+    args.residency = {"dense_gb": round(dense / 1e9, 1), "resident_gb": round(resident / 1e9, 1)} if dense else None
     return pf, plan, slides
 
 
@@ -191,9 +223,16 @@ def make_feed(args, pf, plan, slides, rank, src_size=224, n_local=8, patch=224):
     scfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=mpps, seed=plan.sampler_seed)
     mc = MultiCropConfig(n_local=n_local)
     loader = MultiCropLoader(slides, scfg, mc, batch_size=args.batch, rank=rank, dtype=args.dtype)
-    tag = {"2": "C2", "3": "C3 (mpp U{0.25,0.5,1,2})", "5": f"C5 point (patch {patch}->224, L={n_local})"}[args.config]
-    wl = (f"{tag}: {args.slides} slides {args.width}x{args.height} per GPU in HBM, sat>0.07+morph mask on 1/32 "
-          f"thumbnail, epoch_stream sampler 224px min_fg 0.40, DINOv2 multi-crop 2x224 + {n_local}x96 {args.dtype} NCHW")
+    tag = {"2": "C2", "3": "C3 (mpp U{0.25,0.5,1,2})", "4": "C4", "5": f"C5 point (patch {patch}->224, L={n_local})"}[args.config]
+    if args.config == "4":
+        r = getattr(args, "residency", None) or {}
+        wl = (f"C4: 16 slides per GPU of W~U[40000,100000] x H~U[30000,80000] (128-slide set, seed 4), pyramids "
+              f"{r.get('dense_gb')} GB dense -> {r.get('resident_gb')} GB HBM-resident (tiles reachable from the "
+              f"foreground mask), sat>0.07+morph mask on 1/32 thumbnail, epoch_stream sampler 224px min_fg 0.40, "
+              f"Philox(seed, rank, step) crops, DINOv2 multi-crop 2x224 + {n_local}x96 {args.dtype} NCHW")
+    else:
+        wl = (f"{tag}: {args.slides} slides {args.width}x{args.height} per GPU in HBM, sat>0.07+morph mask on 1/32 "
+              f"thumbnail, epoch_stream sampler 224px min_fg 0.40, DINOv2 multi-crop 2x224 + {n_local}x96 {args.dtype} NCHW")
     return Feed(loader, "multicrop", mc.bytes_per_patch(args.dtype), "multicrop_kernel (global + local crop launches)",
                 wl, run_e2e_multicrop)
 

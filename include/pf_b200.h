@@ -66,9 +66,16 @@ enum pf_mask_mode {
 /* Edge tiles keep the full tile_size^2 footprint; the bytes beyond          */
 /* width/height are never read.  The tile grid is the reference's           */
 /* SlideRecord.tile_grid / tile_dims (pkg/store.py:140-149).                */
+/*                                                                          */
+/* Residency (replaces TileCache/fetch_chunk, pkg/store.py:270-319,          */
+/* 611-649): when tile_map[l] != 0 the level is compacted -- level_ptr[l]    */
+/* holds resident tiles only, as slots of tile_size^2*3 bytes, and           */
+/* tile_map[l] is a device int32[tiles_y*tiles_x] giving tile (tx, ty)'s     */
+/* slot; slot 0 is an all-zero hole that every non-resident tile maps to.    */
 /* ------------------------------------------------------------------------ */
 typedef struct pf_slide_desc {
     uint64_t level_ptr[PF_MAX_LEVELS]; /* device addresses */
+    uint64_t tile_map[PF_MAX_LEVELS];  /* 0: dense level; else device int32 slot map */
     double mpp[PF_MAX_LEVELS];
     int32_t width[PF_MAX_LEVELS];
     int32_t height[PF_MAX_LEVELS];

@@ -42,6 +42,7 @@ PF_AUG_FLIP, PF_AUG_JITTER, PF_AUG_GRAY, PF_AUG_BLUR, PF_AUG_SOLARIZE = 1, 2, 4,
 class SlideDesc(C.Structure):
     _fields_ = [
         ("level_ptr", C.c_uint64 * PF_MAX_LEVELS),
+        ("tile_map", C.c_uint64 * PF_MAX_LEVELS),
         ("mpp", C.c_double * PF_MAX_LEVELS),
         ("width", C.c_int32 * PF_MAX_LEVELS),
         ("height", C.c_int32 * PF_MAX_LEVELS),
@@ -156,7 +157,7 @@ CROP_DTYPE = np.dtype(
 assert CROP_DTYPE.itemsize == 64
 
 assert C.sizeof(SamplerState) == 80
-assert C.sizeof(SlideDesc) == 96 + 96 + 5 * 48 + 8 + 8
+assert C.sizeof(SlideDesc) == 96 + 96 + 96 + 5 * 48 + 8 + 8
 
 
 class _Lib:

@@ -34,15 +34,23 @@ __host__ __device__ inline int64_t rha_nonneg(double x) {
 #endif
 }
 
+// First byte of tile (tx, ty) of a level: dense tile-major, or through the
+// residency slot map (non-resident tiles -> the zero hole slot 0).
+__device__ __forceinline__ const uint8_t* tile_ptr(const pf_slide_desc& s, int level, int tx, int ty) {
+    const size_t tile_bytes = (size_t)s.tile_size * s.tile_size * 3;
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(s.level_ptr[level]);
+    const size_t t = (size_t)ty * s.tiles_x[level] + tx;
+    const int32_t* map = reinterpret_cast<const int32_t*>(s.tile_map[level]);
+    return base + (map ? (size_t)__ldg(map + t) : t) * tile_bytes;
+}
+
 // Address of pixel (X, Y) in a padded tile-major level (see pf_b200.h).
 __device__ __forceinline__ const uint8_t* level_pixel(const pf_slide_desc& s, int level, int X,
                                                       int Y) {
     const int T = s.tile_size;
     const int tx = X / T, ty = Y / T;
     const int u = X - tx * T, v = Y - ty * T;
-    const uint8_t* base = reinterpret_cast<const uint8_t*>(s.level_ptr[level]);
-    const size_t tile_bytes = (size_t)T * T * 3;
-    return base + ((size_t)ty * s.tiles_x[level] + tx) * tile_bytes + ((size_t)v * T + u) * 3;
+    return tile_ptr(s, level, tx, ty) + ((size_t)v * T + u) * 3;
 }
 
 __device__ __forceinline__ uint8_t* level_pixel_mut(const pf_slide_desc& s, int level, int X,

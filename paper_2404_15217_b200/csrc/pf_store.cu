@@ -165,19 +165,18 @@ __device__ int stage_level_rows(const pf_slide_desc& sd, int L, int X0, int Y0, 
                                 int row_bytes, bool fast) {
     const int T = sd.tile_size;
     const int LW = sd.width[L], LH = sd.height[L];
-    const uint8_t* lvl = reinterpret_cast<const uint8_t*>(sd.level_ptr[L]);
     if (fast) {
         const int tx0 = X0 / T, ntx = (X0 + w - 1) / T - tx0 + 1;
         const int cpr = T * 3 / 16;
-        const size_t tile_bytes = (size_t)T * T * 3;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int rr = warp; rr < nr; rr += blockDim.x / 32) {
             const int Y = Y0 + rr;
             const int ty = Y / T, v = Y - ty * T;
-            const uint8_t* grow = lvl + ((size_t)ty * sd.tiles_x[L] + tx0) * tile_bytes + (size_t)v * T * 3;
             uint8_t* srow = stg + rr * row_bytes;
-            for (int t = 0; t < ntx; ++t)
-                for (int ch = lane; ch < cpr; ch += 32) rr_cp_async16(srow + t * T * 3 + ch * 16, grow + t * tile_bytes + ch * 16);
+            for (int t = 0; t < ntx; ++t) {
+                const uint8_t* grow = tile_ptr(sd, L, tx0 + t, ty) + (size_t)v * T * 3;
+                for (int ch = lane; ch < cpr; ch += 32) rr_cp_async16(srow + t * T * 3 + ch * 16, grow + ch * 16);
+            }
         }
         rr_cp_async_wait_all();
         return (X0 - tx0 * T) * 3;

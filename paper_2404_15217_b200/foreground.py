@@ -136,6 +136,7 @@ def _to_device_rgb(thumbnail):
         t = thumbnail
         if t.device.type != "cuda":
             t = t.cuda()
+        t = t.contiguous()  # the C ABI reads the raw row-major buffer
     else:
         arr = np.asarray(thumbnail)
         if arr.ndim != 3 or arr.shape[2] != 3:

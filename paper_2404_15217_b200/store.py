@@ -166,9 +166,42 @@ class GpuSlide:
 
     def __init__(self, record: SlideRecord, levels, factor: int):
         self.record = record
-        self.levels = levels  # torch uint8 [ty, tx, T, T, 3] per level
+        self.levels = levels  # torch uint8 [ty, tx, T, T, 3] per level (dense) or [slots, T, T, 3]
+        self.tile_maps = [None] * len(levels)  # int32 [ty * tx] slot map for compacted levels
         self.factor = factor
         self.desc = self._make_desc()
+
+    def compact(self, plan) -> None:
+        """Keep only the planned tiles resident (residency.reachable_tiles): each level becomes
+        [1 + n_resident] tile slots (slot 0 = zero hole) plus an int32 slot map; the dense level is
+        freed.  Reads of non-resident tiles return zeros (pf_slide_desc.tile_map)."""
+        torch = N.require_cuda()
+        T = self.record.tile_size
+        for li, keep in enumerate(plan):
+            if self.tile_maps[li] is not None:
+                raise ValueError(f"level {li} is already compacted")
+            nx, ny = self.record.tile_grid(li)
+            keep = np.asarray(keep, dtype=bool)
+            if keep.shape != (ny, nx):
+                raise ValueError(f"plan for level {li} must be ({ny}, {nx})")
+            idx = np.flatnonzero(keep.ravel())
+            slots = torch.empty((len(idx) + 1, T, T, 3), dtype=torch.uint8, device="cuda")
+            slots[0].zero_()
+            src = self.levels[li].view(ny * nx, T, T, 3)
+            for i in range(0, len(idx), 4096):  # bounded temporaries (<= 0.8 GB at T = 256)
+                sel = torch.from_numpy(idx[i:i + 4096]).cuda()
+                slots[1 + i:1 + i + len(sel)] = src[sel]
+            del src
+            m = np.zeros(ny * nx, dtype=np.int32)
+            m[idx] = np.arange(1, len(idx) + 1, dtype=np.int32)
+            self.levels[li] = slots
+            self.tile_maps[li] = torch.from_numpy(m).cuda()
+        self.desc = self._make_desc()
+        self._own_set = None
+
+    @property
+    def compacted(self) -> bool:
+        return any(m is not None for m in self.tile_maps)
 
     # -- construction -----------------------------------------------------
     @classmethod
@@ -252,6 +285,8 @@ class GpuSlide:
         for i, lv in enumerate(rec.levels):
             nx, ny = rec.tile_grid(i)
             d.level_ptr[i] = int(self.levels[i].data_ptr()) if self.levels else 0
+            tm = self.tile_maps[i] if self.levels else None
+            d.tile_map[i] = int(tm.data_ptr()) if tm is not None else 0
             d.mpp[i] = lv.mpp
             d.width[i] = lv.width
             d.height[i] = lv.height
@@ -269,6 +304,8 @@ class GpuSlide:
 
     def level_array(self, li: int):
         """Level li as a dense (H, W, 3) uint8 device tensor (copy)."""
+        if self.tile_maps[li] is not None:
+            raise ValueError("level is compacted to its resident tiles; no dense view")
         lv = self.record.levels[li]
         t = self.levels[li]
         ny, nx, T = t.shape[0], t.shape[1], t.shape[2]

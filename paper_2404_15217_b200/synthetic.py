@@ -40,7 +40,9 @@ def tissue_field(width: int, height: int, seed: int, coverage: float = 0.40, blo
     f = _gaussian_blur(noise, max(blob_px / cell / 2.0, 0.75))
     f = (f - f.min()) / max(f.max() - f.min(), 1e-12)
     thr = float(np.quantile(f, 1.0 - coverage))
-    return f.astype(np.float32), thr
+    # C order: apply_along_axis leaves the blurred field Fortran-ordered, and the renderer
+    # indexes the raw buffer row-major
+    return np.ascontiguousarray(f, dtype=np.float32), thr
 
 
 def synthetic_slide(slide_id: str, width: int, height: int, *, seed: int = 0, base_mpp: float = 0.25,
@@ -50,7 +52,7 @@ def synthetic_slide(slide_id: str, width: int, height: int, *, seed: int = 0, ba
     torch = N.require_cuda()
     slide = GpuSlide.allocate(slide_id, width, height, base_mpp, tile_size, downsample_factor)
     field, thr = tissue_field(width, height, seed, coverage, blob_px)
-    fdev = torch.from_numpy(field).cuda()
+    fdev = torch.from_numpy(np.ascontiguousarray(field)).cuda().contiguous()
     N.check(N.lib().pf_synth_level0(slide.desc, fdev.data_ptr(), field.shape[0], field.shape[1], FIELD_CELL,
                                     float(thr), int(seed) & ((1 << 64) - 1), N.stream_ptr(stream)),
             "pf_synth_level0")
