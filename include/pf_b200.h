@@ -233,6 +233,13 @@ typedef struct pf_sampler_state {
     int64_t _reserved;
 } pf_sampler_state;
 
+/* Capped replay draws (replaces CappedCache.draw inside capped_stream,
+ * pkg/sampler.py:230-281): out[i] = stored[randrange(n_stored)] with the
+ * "cache" RandomStream (key = stream key of (seed, "cache")); *counter_dev is
+ * the stream's draw counter, advanced on device (rejections included). */
+int pf_capped_draw(uint64_t key, uint64_t* counter_dev, const pf_patch_spec* stored_dev, int32_t n_stored,
+                   int32_t n, pf_patch_spec* out_dev, void* stream);
+
 /* Bytes of device workspace pf_sample needs for a speculation window. */
 int pf_sample_workspace_bytes(const pf_sampler_config* cfg, int32_t window, int64_t* bytes);
 

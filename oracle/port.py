@@ -331,6 +331,28 @@ def epoch_stream(slides, *, patch_size=256, min_fg=0.40, mpps=((0.25, 1.0),), se
     return out, (s_slide.n, s_coords.n, s_mpp.n)
 
 
+def capped_stream(items, cap, seed: int, total=None) -> list:
+    """capped_stream over a finite list (sampler.py:230-281): the first `cap` items pass through
+    and are retained; then each output is retained[randrange(len)] from Stream(seed, "cache")."""
+    out = []
+    if cap is None:
+        return list(items if total is None else items[:total])
+    kept = []
+    for it in items:
+        if total is not None and len(out) >= total:
+            return out
+        if len(kept) >= cap:
+            break
+        kept.append(it)
+        out.append(it)
+    s = Stream(seed, "cache")
+    while total is None or len(out) < total:
+        out.append(kept[s.randrange(len(kept))])
+        if total is None and len(out) > 10 ** 6:
+            break
+    return out
+
+
 # ---------------------------------------------------------------------------
 # antialiased bilinear resamplers (PIL Resample.c / torch uint8 AA), restated
 

@@ -41,9 +41,12 @@ from .pipeline import (
     write_patch_pack,
 )
 from .sampler import (
+    CappedCache,
+    CappedSampler,
     GpuSampler,
     PatchSpec,
     SamplerConfig,
+    capped_stream,
     epoch_stream,
     footprint_px,
     grid_positions,

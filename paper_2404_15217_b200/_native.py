@@ -194,6 +194,7 @@ class _Lib:
                 [C.POINTER(SamplerConfig), vp, vp, vp, i32, vp, vp, i64, i32, i32, i32, vp],
                 C.c_int,
             ),
+            "pf_capped_draw": ([u64, vp, vp, i32, i32, vp, vp], C.c_int),
             "pf_crop_params": ([u64, i32, u64, i32, C.POINTER(MultiCropConfig), vp, vp], C.c_int),
             "pf_multicrop": (
                 [vp, vp, vp, i32, vp, C.POINTER(MultiCropConfig), i32, vp, vp, vp, vp, vp],

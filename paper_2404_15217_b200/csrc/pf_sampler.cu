@@ -400,6 +400,40 @@ __global__ void sample_begin_kernel(pf_sampler_state* state) {
     state->status = PF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Capped replay (pkg/sampler.py:230-281): output i = stored[randrange(n_stored)] from
+// the "cache" stream, draws consumed in order.  One block: every thread draws for its
+// outputs at counters c0 + 1 + i; a rejected draw (v >= floor(2^64/n)*n, probability
+// n/2^64) shifts all later counters, so then one thread redoes the batch serially.
+// ---------------------------------------------------------------------------
+__global__ void capped_draw_kernel(uint64_t key, uint64_t* counter, const pf_patch_spec* stored, int n_stored,
+                                   int n, pf_patch_spec* out) {
+    __shared__ int any_reject;
+    const uint64_t c0 = *counter;
+    const uint64_t lim = randrange_limit((uint64_t)n_stored);
+    if (threadIdx.x == 0) any_reject = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (!randrange_accepts(stream_u64(key, c0 + 1 + (uint64_t)i), lim)) any_reject = 1;
+    __syncthreads();
+    if (!any_reject) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            out[i] = stored[stream_u64(key, c0 + 1 + (uint64_t)i) % (uint64_t)n_stored];
+        if (threadIdx.x == 0) *counter = c0 + (uint64_t)n;
+        return;
+    }
+    if (threadIdx.x == 0) {
+        uint64_t c = c0;
+        for (int i = 0; i < n; ++i) {
+            uint64_t v;
+            do v = stream_u64(key, ++c);
+            while (!randrange_accepts(v, lim));
+            out[i] = stored[v % (uint64_t)n_stored];
+        }
+        *counter = c;
+    }
+}
+
 }  // namespace pf
 
 using namespace pf;
@@ -479,4 +513,14 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
         if ((rc = after_launch("sample_walk_kernel"))) return rc;
     }
     return PF_OK;
+}
+
+extern "C" int pf_capped_draw(uint64_t key, uint64_t* counter_dev, const pf_patch_spec* stored_dev,
+                              int32_t n_stored, int32_t n, pf_patch_spec* out_dev, void* stream) {
+    if (!counter_dev || n < 0 || (n > 0 && (!out_dev || !stored_dev)))
+        return fail(PF_ERR_INVALID_ARG, "pf_capped_draw: bad arguments");
+    if (n_stored < 1) return fail(PF_ERR_INVALID_ARG, "pf_capped_draw: cannot draw from an empty cache");
+    if (n == 0) return PF_OK;
+    capped_draw_kernel<<<1, 1024, 0, as_stream(stream)>>>(key, counter_dev, stored_dev, n_stored, n, out_dev);
+    return after_launch("capped_draw_kernel");
 }

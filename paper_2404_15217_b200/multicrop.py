@@ -162,9 +162,9 @@ class MultiCropLoader:
 
     def __init__(self, slides, sampler_config, mc_config: MultiCropConfig | None = None, *, batch_size: int = 1024,
                  rank: int = 0, dtype: str = "bf16", mean=IMAGENET_MEAN, std=IMAGENET_STD, window=None, rounds: int = 4,
-                 prefetch: bool = True):
+                 prefetch: bool = True, cap: int | None = None):
         torch = N.require_cuda()
-        from .sampler import GpuSampler
+        from .sampler import CappedSampler, GpuSampler
         from .store import SlideSet
 
         self.mc = mc_config or MultiCropConfig()
@@ -172,6 +172,8 @@ class MultiCropLoader:
             raise ValueError("sampler patch_size must equal the multi-crop source size")
         self.slide_set = SlideSet([s for s, _ in slides])
         self.sampler = GpuSampler(sampler_config, slides, slide_set=self.slide_set, window=window, rounds=rounds)
+        # cap: capped replay of the first `cap` specs (capped_stream, pkg/sampler.py:255-281)
+        self.specs_from = self.sampler if cap is None else CappedSampler(self.sampler, cap, sampler_config.seed)
         self.batch_size = batch_size
         self.rank = rank
         self.seed = sampler_config.seed
@@ -196,7 +198,7 @@ class MultiCropLoader:
                                      dtype=tdt, device="cuda")
 
     def _sample(self, slot: int, st) -> None:
-        self.sampler.next_batch(self.batch_size, out=self.specs_slots[slot], stream=st)
+        self.specs_from.next_batch(self.batch_size, out=self.specs_slots[slot], stream=st)
 
     def next_batch(self, stream=None, marks: list | None = None) -> dict:
         """Enqueue one step and return its device tensors.

@@ -95,6 +95,59 @@ def grid_positions(extent: int, size: int, stride: int) -> list:
     return list(range(0, extent - size + 1, stride))
 
 
+class CappedCache:
+    """Retains the first ``cap`` distinct specs; later draws replay them (pkg/sampler.py:230-252)."""
+
+    def __init__(self, cap: int | None):
+        if cap is not None and cap < 1:
+            raise ValueError("cap must be >= 1 (or None for unlimited)")
+        self.cap = cap
+        self.stored: list = []
+
+    @property
+    def full(self) -> bool:
+        return self.cap is not None and len(self.stored) >= self.cap
+
+    def admit(self, spec) -> None:
+        if self.cap is not None and not self.full:
+            self.stored.append(spec)
+
+    def draw(self, stream) -> "PatchSpec":
+        if not self.stored:
+            raise ValueError("cannot draw from an empty cache")
+        return self.stored[stream.below(len(self.stored))]
+
+
+def capped_stream(inner, cap: int | None, seed_or_stream, total: int | None = None):
+    """Drop-in capped_stream (pkg/sampler.py:255-281): the first ``cap`` items pass through and
+    are retained, afterwards every item is drawn uniformly from the retained set with the
+    (seed, "cache") stream and the inner stream is not advanced.  ``seed_or_stream``: the seed of
+    the reference's ``RandomStream(seed, "cache")`` or an ``rng.Stream``."""
+    from . import rng
+
+    stream = seed_or_stream if isinstance(seed_or_stream, rng.Stream) else rng.Stream(int(seed_or_stream), "cache")
+    cache = CappedCache(cap)
+    count = 0
+    if cap is None:
+        for item in inner:
+            if total is not None and count >= total:
+                return
+            yield item
+            count += 1
+        return
+    for item in inner:
+        if total is not None and count >= total:
+            return
+        if cache.full:
+            break
+        cache.admit(item)
+        yield item
+        count += 1
+    while total is None or count < total:
+        yield cache.draw(stream)
+        count += 1
+
+
 def write_manifest(specs, path) -> int:
     n = 0
     with open(Path(path), "w", encoding="utf-8") as fh:
@@ -303,3 +356,43 @@ def epoch_stream(config: SamplerConfig, slides, batch: int = 4096):
             smp.check()
         smp.update_estimate()
         left -= n
+
+
+class CappedSampler:
+    """Device capped replay over a ``GpuSampler`` (capped_stream, pkg/sampler.py:255-281):
+    the first ``cap`` specs come from the sampler and are kept in HBM; every later spec is a
+    stored spec drawn with the (seed, "cache") stream on device (pf_capped_draw), so the
+    sampler is no longer advanced.  ``next_batch`` returns [n, 64] device spec records, the
+    same stream as the host ``capped_stream``."""
+
+    def __init__(self, sampler: GpuSampler, cap: int, seed: int):
+        torch = N.require_cuda()
+        from . import rng
+
+        if cap < 1:
+            raise ValueError("cap must be >= 1")
+        self.sampler, self.cap = sampler, int(cap)
+        self.key = rng.stream_key(int(seed), "cache")
+        self.stored = torch.empty((self.cap, 64), dtype=torch.uint8, device="cuda")
+        self.n_stored = 0
+        self.counter = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    @property
+    def full(self) -> bool:
+        return self.n_stored >= self.cap
+
+    def next_batch(self, n: int, out=None, stream=None):
+        torch = N.require_cuda()
+        if out is None:
+            out = torch.empty((n, 64), dtype=torch.uint8, device="cuda")
+        k = min(n, self.cap - self.n_stored)
+        if k > 0:  # pass-through and retain
+            fresh = self.sampler.next_batch(k, stream=stream)
+            with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+                self.stored[self.n_stored:self.n_stored + k].copy_(fresh)
+                out[:k].copy_(fresh)
+            self.n_stored += k
+        if n - k > 0:
+            N.check(N.lib().pf_capped_draw(self.key, self.counter.data_ptr(), self.stored.data_ptr(), self.n_stored,
+                                           n - k, out[k:].data_ptr(), N.stream_ptr(stream)), "pf_capped_draw")
+        return out

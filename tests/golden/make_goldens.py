@@ -205,6 +205,14 @@ def main():
             "max_attempts_per_slide")}, "specs": [json.loads(s.to_json_line()) for s in specs]}
     out["epoch_streams"] = man
 
+    # ---- capped replay (pkg/sampler.py:230-281) over the multi_mpp stream
+    base = [sampler.PatchSpec(**d) for d in man["multi_mpp"]["specs"]]
+    cap = {}
+    for c, total, seed in ((7, 40, 13), (1, 9, 2), (25, 60, 13), (None, 20, 13)):
+        got = list(sampler.capped_stream(iter(base), c, rng.RandomStream(seed, "cache"), total=total))
+        cap[f"{c}/{total}/{seed}"] = [s.seq for s in got]
+    out["capped_streams"] = cap
+
     # ---- pipeline
     out["normalize"] = [float(v) for v in pipeline.normalize_patch(np.array([0, 255, 128, 1, 254], np.uint8))]
 

@@ -96,3 +96,19 @@ def test_determinism_and_seed_sensitivity(pf, goldens):
     d = list(pf.epoch_stream(pf.SamplerConfig(patch_size=32, epoch_size=50, seed=2), sl))
     assert a == b and a != d
     assert c["cfg"]["seed"] == 0
+
+
+@pytest.mark.parametrize("key", ["7/40/13", "25/60/13", "1/9/2"])
+def test_capped_replay_on_device_matches_reference(pf, goldens, key):
+    """CappedSampler (pf_capped_draw) over the device sampler reproduces the reference's
+    capped_stream seq sequence across batch boundaries."""
+    cap, total, seed = (int(v) for v in key.split("/"))
+    c = goldens["epoch_streams"]["multi_mpp"]
+    smp = pf.GpuSampler(_cfg(pf, c), _slides(pf, goldens, c["slides"]))
+    cs = pf.CappedSampler(smp, cap, seed)
+    got = []
+    for n in (3, 5, 11, 64):
+        if len(got) >= total:
+            break
+        got += [s.seq for s in smp.to_patch_specs(cs.next_batch(min(n, total - len(got))))]
+    assert got == goldens["capped_streams"][key]

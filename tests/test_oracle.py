@@ -147,3 +147,21 @@ def test_epoch_stream(goldens, case):
 
 def test_normalize(goldens):
     assert port.normalize_patch(np.array([0, 255, 128, 1, 254], np.uint8)).tolist() == goldens["normalize"]
+
+
+def test_capped_stream_oracle_and_host_vs_reference(goldens):
+    """capped_stream (pkg/sampler.py:230-281) over the multi_mpp manifest: the oracle restatement
+    and the package's host mirror both replay the reference's seq sequence."""
+    from paper_2404_15217_b200 import sampler as S
+
+    specs = [S.PatchSpec(**d) for d in goldens["epoch_streams"]["multi_mpp"]["specs"]]
+    for key, want in goldens["capped_streams"].items():
+        cap, total, seed = key.split("/")
+        cap = None if cap == "None" else int(cap)
+        total, seed = int(total), int(seed)
+        assert [s.seq for s in port.capped_stream(specs, cap, seed, total)] == want, key
+        assert [s.seq for s in S.capped_stream(iter(specs), cap, seed, total)] == want, key
+    import pytest
+
+    with pytest.raises(ValueError):
+        S.CappedCache(0)
