@@ -54,6 +54,6 @@ from .sampler import (
     validate_spec,
     write_manifest,
 )
-from .store import GpuSlide, LevelInfo, SlideRecord, SlideSet, round_half_away, select_level
+from .store import GpuSlide, LevelInfo, SlideRecord, SlideSet, ingest_image, round_half_away, select_level
 
 __version__ = "0.1.0"

@@ -364,6 +364,92 @@ def _read_chunk(root: Path, loc: dict, tw: int, th: int) -> np.ndarray:
     return arr
 
 
+CODECS = ("raw", "png", "jpeg")
+_CODEC_EXT = {"raw": ".raw", "png": ".png", "jpeg": ".jpg"}
+
+
+def encode_tile(arr: np.ndarray, codec: str) -> bytes:
+    """encode_tile (pkg/store.py:416-426): raw bytes, or Pillow PNG / JPEG q90."""
+    if codec == "raw":
+        return np.ascontiguousarray(arr).tobytes()
+    import io
+
+    from PIL import Image
+
+    buf = io.BytesIO()
+    Image.fromarray(np.ascontiguousarray(arr)).save(buf, format="PNG" if codec == "png" else "JPEG",
+                                                    **({"quality": 90} if codec == "jpeg" else {}))
+    return buf.getvalue()
+
+
+def _write_json(path: Path, doc: dict) -> None:
+    path.parent.mkdir(parents=True, exist_ok=True)
+    path.write_text(json.dumps(doc, indent=2), encoding="utf-8")
+
+
+def ingest_image(pixels, slide_id: str, base_mpp: float, store_root, *, tile_size: int = 256,
+                 downsample_factor: int = 2, codec: str = "png", layout: str = "files", return_slide: bool = False):
+    """Drop-in ingest_image (pkg/store.py:462-565) with the pyramid built on the GPU.
+
+    Level 0 is uploaded once, levels 1.. come from pf_build_level (the reference's
+    _box_downsample, bit-exact), and the tiles are written in the reference's on-disk format
+    (SPEC.md:113): per-tile files or one packed blob with byte-range locators, the slide
+    record JSON and the store index.  Returns the SlideRecord (and the HBM-resident GpuSlide
+    with ``return_slide``)."""
+    if codec not in CODECS:
+        raise ValueError(f"codec must be one of {CODECS}")
+    if layout not in ("files", "packed"):
+        raise ValueError("layout must be 'files' or 'packed'")
+    slide = GpuSlide.from_array(pixels, slide_id, base_mpp, tile_size=tile_size,
+                                downsample_factor=downsample_factor)
+    rec = SlideRecord(slide_id, base_mpp, tile_size, list(slide.record.levels))
+    root = Path(store_root)
+    T = tile_size
+    try:
+        pack_fh = None
+        pack_rel = f"chunks/{slide_id}.bin"
+        if layout == "packed":
+            (root / pack_rel).parent.mkdir(parents=True, exist_ok=True)
+            pack_fh = open(root / pack_rel, "wb")
+        offset = 0
+        for li in range(len(rec.levels)):
+            nx, ny = rec.tile_grid(li)
+            host = slide.levels[li].cpu().numpy()  # [ty, tx, T, T, 3] padded tiles
+            for ty in range(ny):
+                for tx in range(nx):
+                    tw, th = rec.tile_dims(li, tx, ty)
+                    data = encode_tile(host[ty, tx, :th, :tw], codec)
+                    if layout == "files":
+                        rel = f"chunks/{slide_id}/{li}/{tx}_{ty}{_CODEC_EXT[codec]}"
+                        (root / rel).parent.mkdir(parents=True, exist_ok=True)
+                        (root / rel).write_bytes(data)
+                        loc = {"kind": "inline-file", "path": rel, "codec": codec}
+                    else:
+                        pack_fh.write(data)
+                        loc = {"kind": "byte-range", "path": pack_rel, "codec": codec, "offset": offset,
+                               "length": len(data)}
+                        offset += len(data)
+                    rec.chunks[(li, tx, ty)] = loc
+        if pack_fh is not None:
+            pack_fh.close()
+    except OSError as exc:
+        raise StoreError(f"cannot write chunks under {root}: {exc}") from exc
+    rec.validate()
+    try:
+        _write_json(root / "slides" / f"{slide_id}.json", rec.to_json_dict())
+        idx_path = root / "index.json"
+        index = json.loads(idx_path.read_text(encoding="utf-8")) if idx_path.exists() else {
+            "format_version": STORE_FORMAT_VERSION, "slides": [], "records": {}}
+        if slide_id not in index["slides"]:
+            index["slides"].append(slide_id)
+        index["records"][slide_id] = f"slides/{slide_id}.json"
+        _write_json(idx_path, {"format_version": index["format_version"], "slides": index["slides"],
+                               "records": index["records"]})
+    except OSError as exc:
+        raise StoreError(f"cannot write metadata under {root}: {exc}") from exc
+    return (rec, slide) if return_slide else rec
+
+
 def plan_specs(requests, records) -> np.ndarray:
     """Host read plan for explicit region requests.
 

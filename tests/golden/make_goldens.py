@@ -213,6 +213,15 @@ def main():
         cap[f"{c}/{total}/{seed}"] = [s.seq for s in got]
     out["capped_streams"] = cap
 
+    # ---- ingest_image on-disk format (pkg/store.py:462-565): sha256 of every written file
+    ing = {}
+    for codec, layout in (("raw", "packed"), ("png", "files"), ("jpeg", "packed")):
+        with tempfile.TemporaryDirectory() as td:
+            store.ingest_image(img, "s0", 0.25, td, tile_size=128, downsample_factor=2, codec=codec, layout=layout)
+            ing[f"{codec}/{layout}"] = {str(p.relative_to(td)): hashlib.sha256(p.read_bytes()).hexdigest()
+                                        for p in sorted(Path(td).rglob("*")) if p.is_file()}
+    out["ingest_sha256"] = ing
+
     # ---- pipeline
     out["normalize"] = [float(v) for v in pipeline.normalize_patch(np.array([0, 255, 128, 1, 254], np.uint8))]
 

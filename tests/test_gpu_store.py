@@ -133,3 +133,23 @@ def test_store_roundtrip_from_reference_format(pf, tmp_path, golden_arrays):
         assert np.array_equal(s.level_array(li).cpu().numpy(), a)
     with pytest.raises(pf.SlideNotFoundError):
         pf.GpuSlide.from_store(root, "nope")
+
+
+@pytest.mark.parametrize("codec,layout", [("raw", "packed"), ("png", "files"), ("jpeg", "packed")])
+def test_ingest_image_writes_the_reference_store(cuda, golden_arrays, goldens, tmp_path, codec, layout):
+    """ingest_image with the GPU pyramid writes byte-identical files (tiles, record, index) to the
+    reference's ingest_image on the same image (sha256 of every file)."""
+    import hashlib
+
+    import paper_2404_15217_b200 as pf
+
+    img = golden_arrays["synthetic_700x500"]
+    rec, slide = pf.store.ingest_image(img, "s0", 0.25, tmp_path, tile_size=128, downsample_factor=2, codec=codec,
+                                       layout=layout, return_slide=True)
+    got = {str(p.relative_to(tmp_path)): hashlib.sha256(p.read_bytes()).hexdigest()
+           for p in sorted(tmp_path.rglob("*")) if p.is_file()}
+    assert got == goldens["ingest_sha256"][f"{codec}/{layout}"]
+    if codec != "jpeg":  # lossless: the store reads back to the same resident pyramid
+        back = pf.GpuSlide.from_store(tmp_path, "s0")
+        for li in range(len(rec.levels)):
+            assert cuda.equal(back.level_array(li), slide.level_array(li))
