@@ -231,13 +231,11 @@ class MultiCropLoader:
                 self._ready[cur].record(self._side)
             st.wait_event(self._ready[cur])
             mark("sample_wait")
-            nxt = 1 - cur
-            self._side.wait_event(self._free[nxt])  # step k-1 finished reading that slot
-            self._sample(nxt, self._side)
-            self._ready[nxt] = torch.cuda.Event()
-            self._ready[nxt].record(self._side)
-            self._next_slot = nxt
         specs = self.specs_slots[cur]
+        # the crop parameters (and the resample) are launched before the next step's sampler so
+        # that the sampler's speculative-evaluation blocks do not take the SMs first
+        crop_params(self.mc, n, self.seed, self.rank, self.step, out=self.params, stream=st)
+        mark("params")
         if self.needs_resample:
             m = (C.c_float * 3)(0.5, 0.5, 0.5)
             N.check(N.lib().pf_read_regions(self.slide_set.descs.data_ptr(), specs.data_ptr(), n, self.mc.src_size,
@@ -245,8 +243,13 @@ class MultiCropLoader:
                                             C.cast(m, C.c_void_p), self.src.data_ptr(), N.stream_ptr(st)),
                     "pf_read_regions")
             mark("resample")
-        crop_params(self.mc, n, self.seed, self.rank, self.step, out=self.params, stream=st)
-        mark("params")
+        if self.prefetch:
+            nxt = 1 - cur
+            self._side.wait_event(self._free[nxt])  # step k-1 finished reading that slot
+            self._sample(nxt, self._side)
+            self._ready[nxt] = torch.cuda.Event()
+            self._ready[nxt].record(self._side)
+            self._next_slot = nxt
         multicrop(self.slide_set, specs, self.params, self.mc, dtype=self.dtype, mean=self.mean, std=self.std,
                   src_hwc=self.src, out_global=self.out_global, out_local=self.out_local, stream=st)
         mark("multicrop")
