@@ -146,11 +146,61 @@ __host__ __device__ constexpr int overlap_smem_bytes(int grid) {
     return (2 * grid + 1) * overlap_words(grid) * 4;
 }
 
+// Covered cells of lattice cell rows [r_lo, r_hi): corner rows r_lo..r_hi and centre rows
+// r_lo..r_hi-1 are traced into `smem`, then counted.  With stop >= 0 the rows are taken in
+// chunks of 32 and the count returns early once it reaches `stop` or can no longer reach it
+// (the returned value is then only compared against `stop`).
+__device__ inline int warp_overlap_rows(const PolyView& P, double x, double y, double sx, double sy, int grid,
+                                        uint32_t* smem, int r_lo, int r_hi, int stop) {
+    const int lane = threadIdx.x & 31;
+    const int nw = overlap_words(grid);
+    const int chunk = stop >= 0 ? 32 : grid;
+    uint32_t* corner = smem;                    // chunk + 1 rows
+    uint32_t* centre = smem + (chunk + 1) * nw;  // chunk rows
+    uint32_t words[kMaxWords];
+    int total = 0;
+    for (int c0 = r_lo; c0 < r_hi; c0 += chunk) {
+        const int nrow = min(chunk, r_hi - c0);
+        const int n_rows = 2 * nrow + 1;
+        for (int ri = lane; ri < n_rows; ri += 32) {
+            const bool is_centre = ri > nrow;
+            const int r = is_centre ? ri - nrow - 1 : ri;
+            const double py = lattice(y, sy, c0 + r, is_centre);
+            row_mask(P, py, x, sx, is_centre, is_centre ? grid : grid + 1, nw, words);
+            uint32_t* dst = (is_centre ? centre + r * nw : corner + r * nw);
+            for (int j = 0; j < nw; ++j) dst[j] = words[j];
+        }
+        __syncwarp();
+        int count = 0;
+        for (int r = lane; r < nrow; r += 32) {
+            const uint32_t* cr0 = corner + r * nw;
+            const uint32_t* cr1 = corner + (r + 1) * nw;
+            const uint32_t* m = centre + r * nw;
+            for (int j = 0; j * 32 < grid; ++j) {
+                const uint32_t a = cr0[j], b = cr1[j];
+                const uint32_t a_next = (j + 1 < nw) ? cr0[j + 1] : 0u;
+                const uint32_t b_next = (j + 1 < nw) ? cr1[j + 1] : 0u;
+                const uint32_t a1 = (a >> 1) | (a_next << 31);
+                const uint32_t b1 = (b >> 1) | (b_next << 31);
+                const int rem = grid - 32 * j;
+                const uint32_t valid = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+                count += __popc(a & a1 & b & b1 & m[j] & valid);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
+        __syncwarp();
+        total += count;
+        if (stop >= 0 && (total >= stop || total + (r_hi - c0 - nrow) * grid < stop)) break;
+    }
+    return total;
+}
+
 // Warp-cooperative overlap_fraction numerator: number of covered cells, or
 // -1 when the bounding-box early-out returns 0.0.  All lanes return the same
 // value.  `smem` holds overlap_smem_bytes(grid) for this warp.
-__device__ inline int warp_overlap_count(const PolyView& P, double x, double y, double w, double h,
-                                         int grid, uint32_t* smem) {
+__device__ inline int warp_overlap_count_upto(const PolyView& P, double x, double y, double w, double h,
+                                              int grid, uint32_t* smem, int stop) {
     if (x >= P.bx1 || y >= P.by1 || __dadd_rn(x, w) <= P.bx0 || __dadd_rn(y, h) <= P.by0) return -1;
     const int lane = threadIdx.x & 31;
     const int nw = overlap_words(grid);
@@ -193,39 +243,32 @@ __device__ inline int warp_overlap_count(const PolyView& P, double x, double y, 
         par_and = __all_sync(0xffffffffu, par_and);
         if (!amb && (par_or == 0 || (par_and && !rows_outside))) return par_or ? grid * grid : 0;
     }
-    uint32_t* corner = smem;                      // (grid+1) rows
-    uint32_t* centre = smem + (grid + 1) * nw;    // grid rows
-    const int n_rows = 2 * grid + 1;
-    uint32_t words[kMaxWords];
-    for (int ri = lane; ri < n_rows; ri += 32) {
-        const bool is_centre = ri > grid;
-        const int r = is_centre ? ri - grid - 1 : ri;
-        const double py = lattice(y, sy, r, is_centre);
-        row_mask(P, py, x, sx, is_centre, is_centre ? grid : grid + 1, nw, words);
-        uint32_t* dst = (is_centre ? centre + r * nw : corner + r * nw);
-        for (int j = 0; j < nw; ++j) dst[j] = words[j];
-    }
-    __syncwarp();
-    int count = 0;
-    for (int r = lane; r < grid; r += 32) {
-        const uint32_t* c0 = corner + r * nw;
-        const uint32_t* c1 = corner + (r + 1) * nw;
-        const uint32_t* m = centre + r * nw;
-        for (int j = 0; j * 32 < grid; ++j) {
-            const uint32_t a = c0[j], b = c1[j];
-            const uint32_t a_next = (j + 1 < nw) ? c0[j + 1] : 0u;
-            const uint32_t b_next = (j + 1 < nw) ? c1[j + 1] : 0u;
-            const uint32_t a1 = (a >> 1) | (a_next << 31);
-            const uint32_t b1 = (b >> 1) | (b_next << 31);
-            const int rem = grid - 32 * j;
-            const uint32_t valid = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
-            count += __popc(a & a1 & b & b1 & m[j] & valid);
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
-    __syncwarp();
-    return count;
+    return warp_overlap_rows(P, x, y, sx, sy, grid, smem, 0, grid, stop);
+}
+
+__device__ inline int warp_overlap_count(const PolyView& P, double x, double y, double w, double h, int grid,
+                                         uint32_t* smem) {
+    return warp_overlap_count_upto(P, x, y, w, h, grid, smem, -1);
+}
+
+// Smallest covered-cell count c with c / grid^2 >= min_fg in the reference's FP64 arithmetic
+// (the division it performs, so the comparison is exact); grid^2 + 1 if none.
+__device__ inline int accept_cells(int grid, double min_fg) {
+    const double g2 = (double)grid * (double)grid;
+    int c = (int)fmax(0.0, fmin(g2, ceil(min_fg * g2)));
+    while (c > 0 && __ddiv_rn((double)(c - 1), g2) >= min_fg) --c;
+    while (c <= (int)g2 && !(__ddiv_rn((double)c, g2) >= min_fg)) ++c;
+    return c;
+}
+
+// overlap_fraction(rect) >= min_fg, decided without finishing the lattice when the covered
+// cells so far already reach the threshold, or the rows left cannot (the sampler only needs
+// the acceptance bit, pkg/sampler.py:174-179).  All lanes return the same value.
+__device__ inline bool warp_overlap_accept(const PolyView& P, double x, double y, double w, double h, int grid,
+                                           uint32_t* smem, double min_fg) {
+    const int need = accept_cells(grid, min_fg);
+    const int c = warp_overlap_count_upto(P, x, y, w, h, grid, smem, need);
+    return c < 0 ? 0.0 >= min_fg : c >= need;  // c < 0: bbox early-out, fraction 0.0
 }
 
 }  // namespace pf

@@ -131,11 +131,11 @@ __global__ void sample_eval_kernel(pf_sampler_config cfg, const pf_sampler_slide
     const int y = sl.y_lo[mi] + (int)(vy % ny);
     const PolyView P = poly_view(reinterpret_cast<const void*>(sl.poly_blob));
     uint32_t* sm = s_masks + warp_in_block * (overlap_smem_bytes(cfg.grid) / 4);
-    const int c = warp_overlap_count(P, (double)x, (double)y, (double)fp, (double)fp, cfg.grid, sm);
-    const double frac = c < 0 ? 0.0 : __ddiv_rn((double)c, (double)cfg.grid * (double)cfg.grid);
+    const bool accept = warp_overlap_accept(P, (double)x, (double)y, (double)fp, (double)fp, cfg.grid, sm,
+                                            cfg.min_foreground);
     if (lane == 0) {
         ws.cands[(size_t)s * window + a] = make_int4(x, y, mi, 0);
-        if (frac >= cfg.min_foreground)
+        if (accept)
             atomicOr(ws.bitmaps + (size_t)s * (window / 32) + (a >> 5), 1u << (a & 31));
     }
 }
@@ -224,10 +224,10 @@ __device__ inline int slow_attempt(const pf_sampler_config& cfg, const pf_sample
     const int y = sl.y_lo[mi] + (int)(v % ny);
     const PolyView P = poly_view(reinterpret_cast<const void*>(sl.poly_blob));
     const int fp = sl.fp[mi];
-    const int c = warp_overlap_count(P, (double)x, (double)y, (double)fp, (double)fp, cfg.grid, sm);
+    const bool accept = warp_overlap_accept(P, (double)x, (double)y, (double)fp, (double)fp, cfg.grid, sm,
+                                            cfg.min_foreground);
     w.slow += 1;
-    const double frac = c < 0 ? 0.0 : __ddiv_rn((double)c, (double)cfg.grid * (double)cfg.grid);
-    if (frac >= cfg.min_foreground) {
+    if (accept) {
         if ((threadIdx.x & 31) == 0) emit_spec(cfg, sl, descs[s], s, x, y, mi, w.seq, out + w.emitted);
         w.seq += 1;
         w.emitted += 1;
