@@ -83,7 +83,7 @@ __device__ __forceinline__ double lattice(double x0, double step, int k, bool ce
     const double ek = __dadd_rn(x0, __dmul_rn((double)k, step));
     if (!centre) return ek;
     const double ek1 = __dadd_rn(x0, __dmul_rn((double)(k + 1), step));
-    return __ddiv_rn(__dadd_rn(ek, ek1), 2.0);
+    return __dmul_rn(__dadd_rn(ek, ek1), 0.5);  // == / 2.0 exactly (no subnormals here)
 }
 
 // Inside-mask of one lattice row into `words` (nw 32-bit words, bit k =
@@ -120,16 +120,16 @@ __device__ inline void row_mask(const PolyView& P, double py, double x0, double 
             words[j] = rem >= 32 ? 0xffffffffu : (rem > 0 ? ((1u << rem) - 1u) : 0u);
         }
     }
+    const double inv = 1.0 / step;  // estimate only: the walk below is exact
     for (int i = i_lo; i < i_hi; ++i) {
         const double X = edge_x_at(P, __ldg(P.slab_edge + i), py);
-        // c = number of points with px < X (points ascend in k)
-        int lo = 0, hi = n_pts;
-        while (lo < hi) {
-            const int m = (lo + hi) >> 1;
-            if (lattice(x0, step, m, centre) < X) lo = m + 1;
-            else hi = m;
-        }
-        const int c = lo;
+        // c = number of points with px < X (points ascend in k): start from the nearest lattice
+        // index and step until lattice(m) < X <= lattice(m + 1)
+        const double est = floor((X - x0) * inv - (centre ? 0.5 : 0.0));
+        int m = est < -1.0 ? -1 : (est > (double)(n_pts - 1) ? n_pts - 1 : (int)est);
+        while (m >= 0 && !(lattice(x0, step, m, centre) < X)) --m;
+        while (m + 1 < n_pts && lattice(x0, step, m + 1, centre) < X) ++m;
+        const int c = m + 1;
         for (int j = 0; j < nw; ++j) {
             const int rem = c - 32 * j;
             words[j] ^= rem >= 32 ? 0xffffffffu : (rem > 0 ? ((1u << rem) - 1u) : 0u);
