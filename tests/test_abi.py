@@ -139,3 +139,23 @@ def test_struct_layouts_match_header(native, tmp_path):
             native.CROP_DTYPE.itemsize, native.SPEC_DTYPE.fields["sx"][1], native.SamplerState.cur_slide.offset,
             native.CROP_DTYPE.fields["sigma"][1]]
     assert got == want
+
+
+def test_argument_validation_without_device(native):
+    """Every entry point validates before touching CUDA: bad pointers / sizes fail with
+    PF_ERR_INVALID_ARG and a message; empty batches are a no-op success."""
+    L = native.lib()
+    assert L.pf_capped_draw(1, None, None, 1, 4, None, None) == native.PF_ERR_INVALID_ARG
+    assert L.pf_capped_draw(1, 8, 8, 0, 4, 8, None) == native.PF_ERR_INVALID_ARG  # empty cache
+    assert b"empty cache" in L.pf_last_error()
+    assert L.pf_capped_draw(1, 8, 8, 3, 0, None, None) == native.PF_OK
+    assert L.pf_crop_params(0, 0, 0, -1, None, None, None) == native.PF_ERR_INVALID_ARG
+    cfg = native.MultiCropConfig()
+    cfg.n_global, cfg.n_local, cfg.src_size, cfg.global_size, cfg.local_size = 2, 8, 224, 224, 96
+    assert L.pf_crop_params(0, 0, 0, 0, C.byref(cfg), None, None) == native.PF_OK
+    assert L.pf_multicrop(None, None, None, 0, None, C.byref(cfg), 2, None, None, None, None, None) == native.PF_OK
+    cfg.global_size = 100  # not a multiple of 8
+    assert L.pf_multicrop(8, 8, None, 1, 8, C.byref(cfg), 2, None, None, 8, 8, None) == native.PF_ERR_INVALID_ARG
+    assert L.pf_read_regions(8, 8, 0, 224, 0, 0, None, None, 8, None) == native.PF_OK
+    assert L.pf_read_regions(8, 8, 1, 600, 0, 0, None, None, 8, None) == native.PF_ERR_INVALID_ARG
+    assert L.pf_rrc_table_build(224, 32, 8, None) == native.PF_ERR_INVALID_ARG  # down-ratio > 3.5
