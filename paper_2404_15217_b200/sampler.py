@@ -10,6 +10,8 @@ without host round trips between batches (csrc/pf_sampler.cu).
 
 from __future__ import annotations
 
+import math
+
 import ctypes as C
 import json
 from dataclasses import dataclass, field
@@ -282,7 +284,10 @@ class GpuSampler:
     def _window_for(self, n: int) -> int:
         if self.window:
             return max(32, (self.window + 31) // 32 * 32)
-        w = int(1.3 * n / self.p_est) + 64
+        # attempts for n accepts ~ negative binomial: mean n/p, sd sqrt(n(1-p))/p; 3 sd of slack,
+        # further rounds cover the rare overflow (every offset is evaluated for every slide)
+        p = self.p_est
+        w = int(n / p + 3.0 * math.sqrt(n * (1.0 - p)) / p) + 32
         return min(max(32, (w + 31) // 32 * 32), 1 << 16)
 
     def next_batch(self, n: int, out=None, stream=None):
