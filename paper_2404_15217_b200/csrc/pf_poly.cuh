@@ -226,14 +226,9 @@ __device__ inline int warp_overlap_count_upto(const PolyView& P, double x, doubl
                 if (__ldg(P.hi + m) < x) a = m + 1;
                 else b = m;
             }
-            const int i_lo = a;
-            b = e1;
-            while (a < b) {
-                const int m = (a + b) >> 1;
-                if (__ldg(P.lo + m) > xlast) b = m;
-                else a = m + 1;
-            }
-            amb |= i_lo < a;
+            // lo is suffix-min sorted: no edge of [i_lo, e1) starts left of x_last iff lo[i_lo] does
+            // not, and then i_hi == i_lo
+            amb |= a < e1 && !(__ldg(P.lo + a) > xlast);
             const int par = (e1 - a) & 1;
             par_or |= par;
             par_and &= par;
