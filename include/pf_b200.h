@@ -233,6 +233,19 @@ typedef struct pf_sampler_state {
     int64_t _reserved;
 } pf_sampler_state;
 
+/* On-GPU PNG tile decode (replaces decode_tile's Pillow path for the store's
+ * default codec, pkg/store.py:397-416, 470).  pf_png_inflate: one thread per
+ * tile inflates the zlib stream zdata[zoff[t] .. zoff[t+1]) (concatenated IDAT
+ * payloads of an 8-bit RGB non-interlaced PNG) into raw[roff[t] .. +rlen[t]),
+ * rlen = th * (1 + 3 * tw) filtered scanline bytes; status_dev[t] = 0 or a
+ * negative parse error.  pf_png_unfilter: undoes the row filters of tiles
+ * whose status is 0 into dst_dev[t] (a tile slot, row pitch tile_size * 3). */
+int pf_png_inflate(const uint8_t* zdata_dev, const int64_t* zoff_dev, int32_t n, uint8_t* raw_dev,
+                   const int64_t* roff_dev, const int64_t* rlen_dev, int32_t* status_dev, void* stream);
+int pf_png_unfilter(const uint8_t* raw_dev, const int64_t* roff_dev, const int32_t* tile_w_dev,
+                    const int32_t* tile_h_dev, uint8_t* const* dst_dev, int32_t tile_size, int32_t n,
+                    int32_t* status_dev, void* stream);
+
 /* Capped replay draws (replaces CappedCache.draw inside capped_stream,
  * pkg/sampler.py:230-281): out[i] = stored[randrange(n_stored)] with the
  * "cache" RandomStream (key = stream key of (seed, "cache")); *counter_dev is

@@ -195,6 +195,8 @@ class _Lib:
                 C.c_int,
             ),
             "pf_capped_draw": ([u64, vp, vp, i32, i32, vp, vp], C.c_int),
+            "pf_png_inflate": ([vp, vp, i32, vp, vp, vp, vp, vp], C.c_int),
+            "pf_png_unfilter": ([vp, vp, vp, vp, vp, i32, i32, vp, vp], C.c_int),
             "pf_crop_params": ([u64, i32, u64, i32, C.POINTER(MultiCropConfig), vp, vp], C.c_int),
             "pf_multicrop": (
                 [vp, vp, vp, i32, vp, C.POINTER(MultiCropConfig), i32, vp, vp, vp, vp, vp],

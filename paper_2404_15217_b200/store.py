@@ -235,11 +235,14 @@ class GpuSlide:
         return slide
 
     @classmethod
-    def from_store(cls, store_root, slide_id: str, stream=None) -> "GpuSlide":
+    def from_store(cls, store_root, slide_id: str, stream=None, gpu_png: bool = True) -> "GpuSlide":
         """Load a reference store slide (index.json + slides/<id>.json + chunks) into HBM.
 
         Every level is read as stored (raw/png/jpeg via the store's locators) so the
-        HBM pyramid holds the exact bytes the reference serves.
+        HBM pyramid holds the exact bytes the reference serves.  PNG tiles (the store's
+        default codec) are inflated and unfiltered on the GPU (pf_png_inflate /
+        pf_png_unfilter) after a host check of the chunk CRCs; other codecs and PNG
+        variants Pillow writes only for non-RGB images decode on the host.
         """
         torch = N.require_cuda()
         root = Path(store_root)
@@ -262,14 +265,23 @@ class GpuSlide:
         for li, lv in enumerate(rec.levels):
             nx, ny = rec.tile_grid(li)
             host = np.zeros((ny, nx, T, T, 3), dtype=np.uint8)
+            png = []  # (tx, ty, tw, th, zlib stream) decoded on the GPU
             for ty in range(ny):
                 for tx in range(nx):
                     loc = rec.chunks.get((li, tx, ty))
                     if loc is None:
                         raise IntegrityError(f"missing chunk locator ({li}, {tx}, {ty})")
                     tw, th = rec.tile_dims(li, tx, ty)
+                    if gpu_png and loc["codec"] == "png" and tw <= 256:
+                        z = _png_zlib_stream(_read_chunk_bytes(root, loc), tw, th)
+                        if z is not None:
+                            png.append((tx, ty, tw, th, z))
+                            continue
                     host[ty, tx, :th, :tw] = _read_chunk(root, loc, tw, th)
-            levels.append(torch.from_numpy(host).cuda())
+            dev = torch.from_numpy(host).cuda()
+            if png:
+                _decode_png_tiles(dev, T, png, stream)
+            levels.append(dev)
         return cls(rec, levels, factor)
 
     def build_pyramid(self, stream=None) -> None:
@@ -335,18 +347,91 @@ class GpuSlide:
         return out[0].cpu().numpy()
 
 
-def _read_chunk(root: Path, loc: dict, tw: int, th: int) -> np.ndarray:
+def _read_chunk_bytes(root: Path, loc: dict) -> bytes:
     path = loc["path"]
     p = Path(path) if Path(path).is_absolute() else root / path
     try:
         if loc["kind"] == "byte-range":
             with open(p, "rb") as fh:
                 fh.seek(int(loc["offset"]))
-                data = fh.read(int(loc["length"]))
-        else:
-            data = p.read_bytes()
+                return fh.read(int(loc["length"]))
+        return p.read_bytes()
     except OSError as exc:
         raise StoreError(f"cannot read {p}: {exc}") from exc
+
+
+_PNG_SIG = b"\x89PNG\r\n\x1a\n"
+
+
+def _png_zlib_stream(data: bytes, tw: int, th: int):
+    """The zlib stream (concatenated IDAT payloads) of an 8-bit RGB non-interlaced tw x th PNG,
+    every chunk CRC checked; None for any other PNG variant (decoded on the host)."""
+    import struct
+    import zlib
+
+    if data[:8] != _PNG_SIG:
+        raise DecodeError("not a PNG tile")
+    pos, idat, ok = 8, [], False
+    while pos + 12 <= len(data):
+        n = int.from_bytes(data[pos:pos + 4], "big")
+        typ, body = data[pos + 4:pos + 8], data[pos + 8:pos + 8 + n]
+        if len(body) != n or pos + 12 + n > len(data):
+            raise DecodeError("truncated PNG chunk")
+        if zlib.crc32(typ + body) != int.from_bytes(data[pos + 8 + n:pos + 12 + n], "big"):
+            raise DecodeError(f"PNG chunk {typ!r} fails its CRC")
+        if typ == b"IHDR":
+            ok = struct.unpack(">IIBBBBB", body) == (tw, th, 8, 2, 0, 0, 0)
+        elif typ == b"IDAT":
+            idat.append(body)
+        elif typ == b"IEND":
+            break
+        pos += 12 + n
+    return b"".join(idat) if ok and idat else None
+
+
+def _decode_png_tiles(level, T: int, tiles, stream=None, chunk: int = 4096) -> None:
+    """Inflate + unfilter PNG tiles on the GPU into a dense level [ty, tx, T, T, 3] (tiles up to 256
+    px wide; wider tiles decode on the host)."""
+    torch = N.require_cuda()
+    L = N.lib()
+    nx = level.shape[1]
+    tb = T * T * 3
+    for i in range(0, len(tiles), chunk):
+        part = tiles[i:i + chunk]
+        n = len(part)
+        zl = np.array([len(t[4]) for t in part], dtype=np.int64)
+        zoff = np.zeros(n + 1, dtype=np.int64)
+        zoff[1:] = np.cumsum(zl)
+        rlen = np.array([t[3] * (1 + 3 * t[2]) for t in part], dtype=np.int64)
+        roff = np.zeros(n, dtype=np.int64)
+        roff[1:] = np.cumsum(rlen)[:-1]
+        pinned = torch.empty(int(zoff[-1]), dtype=torch.uint8, pin_memory=True)  # one H2D for all streams
+        host = pinned.numpy()
+        for k, t in enumerate(part):
+            host[zoff[k]:zoff[k + 1]] = np.frombuffer(t[4], dtype=np.uint8)
+        zdev = pinned.to("cuda", non_blocking=True)
+        raw = torch.empty(int(rlen.sum()), dtype=torch.uint8, device="cuda")
+        status = torch.zeros(n, dtype=torch.int32, device="cuda")
+        base = int(level.data_ptr())
+        dst = np.array([base + (t[1] * nx + t[0]) * tb for t in part], dtype=np.uint64)
+        dv = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+        zoff_d, roff_d, rlen_d, dst_d = dv(zoff), dv(roff), dv(rlen), dv(dst.view(np.int64))
+        tw_d = dv(np.array([t[2] for t in part], dtype=np.int32))
+        th_d = dv(np.array([t[3] for t in part], dtype=np.int32))
+        sp = N.stream_ptr(stream)
+        N.check(L.pf_png_inflate(zdev.data_ptr(), zoff_d.data_ptr(), n, raw.data_ptr(), roff_d.data_ptr(),
+                                 rlen_d.data_ptr(), status.data_ptr(), sp), "pf_png_inflate")
+        N.check(L.pf_png_unfilter(raw.data_ptr(), roff_d.data_ptr(), tw_d.data_ptr(), th_d.data_ptr(),
+                                  dst_d.data_ptr(), T, n, status.data_ptr(), sp), "pf_png_unfilter")
+        st = status.cpu().numpy()
+        bad = np.flatnonzero(st)
+        if len(bad):
+            t = part[int(bad[0])]
+            raise DecodeError(f"cannot decode png tile ({t[0]}, {t[1]}): inflate/unfilter status {int(st[bad[0]])}")
+
+
+def _read_chunk(root: Path, loc: dict, tw: int, th: int) -> np.ndarray:
+    data = _read_chunk_bytes(root, loc)
     if loc["codec"] == "raw":
         if len(data) != tw * th * 3:
             raise DecodeError(f"raw tile has {len(data)} bytes, expected {tw * th * 3}")
