@@ -192,6 +192,49 @@ __device__ int stage_level_rows(const pf_slide_desc& sd, int L, int X0, int Y0, 
     return 0;
 }
 
+// PIL horizontal pass of one output column over staged rows [rr0, rr1) (22-bit int taps,
+// planar uint8 out).  K > 0: taps unrolled and kept in registers (zero beyond xsize).
+template <int K>
+__device__ __forceinline__ void pil_h_rows(const uint8_t* stg, int pitch, int off, int xmin, int xs, const int32_t* w,
+                                           int rr0, int rr1, uint8_t* hb_col, int S, int hplane) {
+    const uint8_t* s0 = stg + off + xmin * 3;
+    if constexpr (K > 0) {
+        int32_t wk[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) wk[k] = k < xs ? w[k] : 0;
+        for (int rr = rr0; rr < rr1; ++rr) {
+            const uint8_t* p = s0 + rr * pitch;
+            int32_t a0 = 1 << 21, a1 = 1 << 21, a2 = 1 << 21;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (k < xs) {  // taps past xsize may lie beyond the staged span
+                    a0 += (int32_t)p[3 * k] * wk[k];
+                    a1 += (int32_t)p[3 * k + 1] * wk[k];
+                    a2 += (int32_t)p[3 * k + 2] * wk[k];
+                }
+            }
+            uint8_t* d = hb_col + rr * S;
+            d[0] = clip_shift(a0, 22);
+            d[hplane] = clip_shift(a1, 22);
+            d[2 * hplane] = clip_shift(a2, 22);
+        }
+    } else {
+        for (int rr = rr0; rr < rr1; ++rr) {
+            const uint8_t* p = s0 + rr * pitch;
+            int32_t a0 = 1 << 21, a1 = 1 << 21, a2 = 1 << 21;
+            for (int k = 0; k < xs; ++k) {
+                a0 += (int32_t)p[3 * k] * w[k];
+                a1 += (int32_t)p[3 * k + 1] * w[k];
+                a2 += (int32_t)p[3 * k + 2] * w[k];
+            }
+            uint8_t* d = hb_col + rr * S;
+            d[0] = clip_shift(a0, 22);
+            d[hplane] = clip_shift(a1, 22);
+            d[2 * hplane] = clip_shift(a2, 22);
+        }
+    }
+}
+
 template <int kDtype>
 struct RROut;
 template <>
@@ -286,7 +329,9 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
         return;
     }
 
-    // ---- PIL resample of the whole window (one CTA per spec)
+    // ---- PIL resample of the whole window (one CTA per spec): fixed output-row bands, the
+    // 16-byte aligned span of each window row staged with cp.async one band ahead, horizontal
+    // pass with the row's taps in registers, vertical pass into the epilogue
     const AxisPlan ap = axis_plan(side, S);
     const int K = ap.ksize;
     int* s_xmin = reinterpret_cast<int*>(work);
@@ -295,50 +340,94 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
     double* s_red = reinterpret_cast<double*>(work + (((size_t)(2 * S + S * K) * 4 + 15) & ~size_t(15)));
     uint8_t* buf = reinterpret_cast<uint8_t*>(s_red + 2);
     const int buf_bytes = work_bytes - (int)(buf - work);
-    build_axis_table(side, S, RS_PIL, s_xmin, s_xsize, s_w, s_red);
+    build_axis_table(side, S, RS_PIL, s_xmin, s_xsize, s_w, s_red);  // ends with __syncthreads
     const int sx = sp.sx, sy = sp.sy;
-    const bool fast_all = sx >= 0 && sy >= 0 && sx + side <= LW && sy + side <= LH && (T % 16) == 0;
-    const int row_bytes = fast_all ? ((sx + side - 1) / T - sx / T + 1) * T * 3 : ((side * 3 + 15) & ~15);
-    const int max_rows = buf_bytes / (row_bytes + 3 * S);
-    int y0 = 0;
-    while (y0 < S) {
-        const int r0 = s_xmin[y0];
-        int y1 = y0 + 1;
-        while (y1 < S && s_xmin[y1] + s_xsize[y1] - r0 <= max_rows) ++y1;
-        const int r1 = s_xmin[y1 - 1] + s_xsize[y1 - 1];
+    const bool fast = sx >= 0 && sy >= 0 && sx + side <= LW && sy + side <= LH && (T % 16) == 0;
+    const int a0 = fast ? (sx * 3) & ~15 : 0;
+    const int off = fast ? sx * 3 - a0 : 0;
+    const int nch = (off + side * 3 + 15) / 16;
+    const int pitch = nch * 16 + 16;
+    const int cap = (buf_bytes - 3 * S * 4) / (2 * pitch + 3 * S);  // source rows per band
+    if (cap < 4) return;  // host checks the window fits (out_size <= 512)
+    uint8_t* hb = buf + 2 * cap * pitch;  // [3][cap + 4][S]
+    const int hplane = (cap + 4) * S;
+    int R = (int)floor(((double)cap - 1.0 - 2.0 * ap.support) / ap.scale) + 1;
+    R = R < 1 ? 1 : (R > S ? S : R);
+    const int nb = (S + R - 1) / R;
+    auto rows_of = [&](int bnd, int& r0, int& r1) {  // axis_weights' own xmin / xmax bounds
+        const int y0 = bnd * R, y1 = min(S, y0 + R);
+        r0 = (int)(ap.scale * ((double)y0 + 0.5) - ap.support + 0.5);
+        r0 = r0 < 0 ? 0 : r0;
+        r1 = (int)(ap.scale * ((double)(y1 - 1) + 0.5) + ap.support + 0.5);
+        r1 = r1 > side ? side : r1;
+    };
+    const int cpr = T * 3 / 16;
+    auto stage = [&](int bnd) {
+        int r0, r1;
+        rows_of(bnd, r0, r1);
         const int nr = r1 - r0;
-        uint8_t* stg = buf;
-        uint8_t* hb = buf + nr * row_bytes;  // [3][nr][S]
-        const int base = stage_level_rows(sd, L, sx, sy + r0, side, nr, stg, row_bytes, fast_all);
-        __syncthreads();
-        for (int q = threadIdx.x; q < nr * S; q += kRRThreads) {
-            const int rr = q / S, x = q - rr * S;
-            const uint8_t* srow = stg + rr * row_bytes + base;
-            const int xmin = s_xmin[x], xs = s_xsize[x];
-            int32_t a0 = 1 << 21, a1 = 1 << 21, a2 = 1 << 21;
-            for (int k = 0; k < xs; ++k) {
-                const uint8_t* p = srow + (xmin + k) * 3;
-                const int32_t wk = s_w[x * K + k];
-                a0 += (int32_t)p[0] * wk;
-                a1 += (int32_t)p[1] * wk;
-                a2 += (int32_t)p[2] * wk;
+        uint8_t* stg = buf + (bnd & 1) * cap * pitch;
+        if (fast) {
+            const int c0 = a0 / 16, tx0 = c0 / cpr, e0 = c0 - tx0 * cpr;
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            for (int rr = warp; rr < nr; rr += kRRThreads / 32) {
+                const int Y = sy + r0 + rr;
+                const int ty = Y / T, v = Y - ty * T;
+                for (int ch = lane; ch < nch; ch += 32) {
+                    const int e = e0 + ch, t = e / cpr;
+                    rr_cp_async16(stg + rr * pitch + ch * 16, tile_ptr(sd, L, tx0 + t, ty) + (size_t)v * T * 3 + (e - t * cpr) * 16);
+                }
             }
-            hb[rr * S + x] = clip_shift(a0, 22);
-            hb[(nr + rr) * S + x] = clip_shift(a1, 22);
-            hb[(2 * nr + rr) * S + x] = clip_shift(a2, 22);
+        } else {  // window touches the level edge: clamped per-pixel gather
+            for (int q = threadIdx.x; q < nr * side; q += kRRThreads) {
+                const int rr = q / side, xx = q - rr * side;
+                const uint8_t* p = level_pixel(sd, L, clampi(sx + xx, 0, LW - 1), clampi(sy + r0 + rr, 0, LH - 1));
+                uint8_t* d = stg + rr * pitch + xx * 3;
+                d[0] = p[0];
+                d[1] = p[1];
+                d[2] = p[2];
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    stage(0);
+    for (int bnd = 0; bnd < nb; ++bnd) {
+        const int y0 = bnd * R, y1 = min(S, y0 + R);
+        int r0, r1;
+        rows_of(bnd, r0, r1);
+        const int nr = r1 - r0;
+        if (bnd + 1 < nb) stage(bnd + 1);
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncthreads();
+        const uint8_t* stg = buf + (bnd & 1) * cap * pitch;
+        // horizontal pass: item = (4 source rows, output column)
+        const int ngr = (nr + 3) >> 2;
+        for (int q = threadIdx.x; q < ngr * S; q += kRRThreads) {
+            const int g = q / S, x = q - g * S;
+            const int rr0 = g * 4, rr1 = min(nr, rr0 + 4);
+            switch (K) {
+                case 3: pil_h_rows<3>(stg, pitch, off, s_xmin[x], s_xsize[x], s_w + x * K, rr0, rr1, hb + x, S, hplane); break;
+                case 5: pil_h_rows<5>(stg, pitch, off, s_xmin[x], s_xsize[x], s_w + x * K, rr0, rr1, hb + x, S, hplane); break;
+                case 7: pil_h_rows<7>(stg, pitch, off, s_xmin[x], s_xsize[x], s_w + x * K, rr0, rr1, hb + x, S, hplane); break;
+                case 9: pil_h_rows<9>(stg, pitch, off, s_xmin[x], s_xsize[x], s_w + x * K, rr0, rr1, hb + x, S, hplane); break;
+                default: pil_h_rows<0>(stg, pitch, off, s_xmin[x], s_xsize[x], s_w + x * K, rr0, rr1, hb + x, S, hplane); break;
+            }
         }
         __syncthreads();
+        // vertical pass -> output rows [y0, y1)
         for (int q = threadIdx.x; q < (y1 - y0) * S; q += kRRThreads) {
             const int yy = q / S, x = q - yy * S;
             const int y = y0 + yy;
             const int ymin = s_xmin[y] - r0, ys = s_xsize[y];
+            const int32_t* wy = s_w + y * K;
             int32_t a[3] = {1 << 21, 1 << 21, 1 << 21};
+            const uint8_t* col = hb + ymin * S + x;
             for (int k = 0; k < ys; ++k) {
-                const int32_t wk = s_w[y * K + k];
-                const int b = (ymin + k) * S + x;
-                a[0] += (int32_t)hb[b] * wk;
-                a[1] += (int32_t)hb[nr * S + b] * wk;
-                a[2] += (int32_t)hb[2 * nr * S + b] * wk;
+                const int32_t wk = wy[k];
+                a[0] += (int32_t)col[k * S] * wk;
+                a[1] += (int32_t)col[hplane + k * S] * wk;
+                a[2] += (int32_t)col[2 * hplane + k * S] * wk;
             }
             for (int c = 0; c < 3; ++c) {
                 const size_t idx = lay == PF_HWC ? ((size_t)y * S + x) * 3 + c : c * plane + (size_t)y * S + x;
@@ -346,7 +435,6 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
             }
         }
         __syncthreads();
-        y0 = y1;
     }
 }
 
