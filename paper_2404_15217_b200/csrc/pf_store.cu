@@ -527,7 +527,9 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
         np.mean[c] = mean3 ? mean3[c] : 0.5f;
         np.stdv[c] = std3 ? std3[c] : 0.5f;
     }
-    const int n_bands = (out_size + kRRBand - 1) / kRRBand;
+    // passthrough specs split into row bands across CTAs; with PF_SKIP_PASSTHROUGH only the
+    // resampled specs do work (one CTA each), so no band CTAs are launched
+    const int n_bands = (layout & PF_SKIP_PASSTHROUGH) ? 1 : (out_size + kRRBand - 1) / kRRBand;
     const long long grid = (long long)n * n_bands;
     cudaStream_t st = as_stream(stream);
     int rc;
