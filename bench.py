@@ -367,6 +367,23 @@ def timed_run(feed, args, torch, dist, world, local, N):
     return float(t.item()), stage_ms, launches, clk.summary()
 
 
+def issue_roofline(args, k_ms):
+    """The bound that binds the multi-crop kernel: instruction issue.  Warp-instructions per patch
+    come from the committed ncu capture (profiles/instr_config<N>.json); the ceiling is one
+    warp-instruction per scheduler per clock: 148 SMs x 4 x sm_max_mhz."""
+    ip = ROOT / "profiles" / f"instr_config{args.config}.json"
+    if not ip.exists():
+        return None
+    try:
+        wipp = float(json.loads(ip.read_text())["warp_instructions_per_patch"])
+    except (ValueError, KeyError):
+        return None
+    peak = 148 * 4 * 1965e6
+    achieved = wipp * args.batch / (k_ms / 1000.0)
+    return {"unit": "warp-instr/s", "achieved": round(achieved, -6), "peak": peak, "frac": round(achieved / peak, 4),
+            "warp_instructions_per_patch": wipp, "source": json.loads(ip.read_text()).get("source")}
+
+
 def result_line(feed, args, world, elapsed_ms, stage_ms, launches, clocks, st, e2e, cpu):
     peak, peak_kind = measured_peak_hbm()
     n_total = args.steps * args.batch * world
@@ -413,6 +430,7 @@ def result_line(feed, args, world, elapsed_ms, stage_ms, launches, clocks, st, e
             "algorithmic_bytes_per_patch": feed.bytes_per_patch,
             "per_launch_ms": round(k_ms, 4),
         },
+        "issue_roofline": issue_roofline(args, k_ms),
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "sampler": {"attempts": int(st.attempts), "specs": int(st.seq), "slow_evals": int(st.slow_evals)},
         "gpu_launches": int(launches),
