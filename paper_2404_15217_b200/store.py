@@ -168,6 +168,7 @@ class GpuSlide:
         self.record = record
         self.levels = levels  # torch uint8 [ty, tx, T, T, 3] per level (dense) or [slots, T, T, 3]
         self.tile_maps = [None] * len(levels)  # int32 [ty * tx] slot map for compacted levels
+        self.resident = [None] * len(levels)  # host bool [ty, tx] of compacted levels
         self.factor = factor
         self.desc = self._make_desc()
 
@@ -196,6 +197,7 @@ class GpuSlide:
             m[idx] = np.arange(1, len(idx) + 1, dtype=np.int32)
             self.levels[li] = slots
             self.tile_maps[li] = torch.from_numpy(m).cuda()
+            self.resident[li] = keep
         self.desc = self._make_desc()
         self._own_set = None
 
@@ -341,6 +343,17 @@ class GpuSlide:
     def read_region(self, rect_level0, target_mpp: float, out_size: int) -> np.ndarray:
         """Drop-in Slide.read_region (pkg/store.py:651-688): (out, out, 3) uint8 host array."""
         specs = plan_specs([(0, rect_level0, target_mpp, out_size)], [self.record])
+        li = int(specs[0]["level"])
+        if self.resident[li] is not None:  # compacted level: the window must lie on resident tiles
+            lv, T = self.record.levels[li], self.record.tile_size
+            x0 = round_half_away(rect_level0[0] / lv.downsample)
+            y0 = round_half_away(rect_level0[1] / lv.downsample)
+            side = int(specs[0]["side"])
+            tx0, ty0 = max(x0, 0) // T, max(y0, 0) // T
+            tx1, ty1 = min(x0 + side - 1, lv.width - 1) // T, min(y0 + side - 1, lv.height - 1) // T
+            if not self.resident[li][ty0:ty1 + 1, tx0:tx1 + 1].all():
+                raise StoreError(f"region {tuple(rect_level0)} reads tiles that are not HBM-resident "
+                                 "(slide compacted to the sampler's reachable tiles)")
         if getattr(self, "_own_set", None) is None:
             self._own_set = SlideSet([self])
         out = self._own_set.read_regions(specs, out_size)

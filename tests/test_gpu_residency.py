@@ -59,7 +59,10 @@ def test_non_resident_tiles_read_as_hole(pf):
     T = s.record.tile_size
     ty, tx = np.argwhere(~plan[0])[0]
     s.compact(plan)
-    px = s.read_region((int(tx) * T + 8, int(ty) * T + 8, 64, 64), 0.25, 64)
-    assert px.shape == (64, 64, 3) and not px.any()
+    with pytest.raises(pf.StoreError):  # the host drop-in refuses non-resident windows
+        s.read_region((int(tx) * T + 8, int(ty) * T + 8, 64, 64), 0.25, 64)
+    specs = pf.store.plan_specs([(0, (int(tx) * T + 8, int(ty) * T + 8, 64, 64), 0.25, 64)], [s.record])
+    px = pf.SlideSet([s]).read_regions(specs, 64)  # the batched device path reads the zero hole
+    assert px.shape == (1, 64, 64, 3) and not px.any()
     with pytest.raises(ValueError):
         s.level_array(0)
