@@ -170,3 +170,27 @@ def test_hue_every_colour_exact(pf):
         want = A.hue(src, float(p["hue"]))
         got = g[0, k].transpose(1, 2, 0)
         assert np.array_equal(got, want), (k, float(p["hue"]), int((got != want).any(-1).sum()))
+
+
+@pytest.mark.parametrize("n_local,local_size", [(0, 96), (4, 112)])
+def test_crop_count_and_size_variants_vs_torchvision(pf, scene, n_local, local_size):
+    """BASELINE config 5 shapes: no local crops, or 4 local crops of another size (generic-size
+    kernel path), against torchvision on the same parameters."""
+    cfg = pf.mc.MultiCropConfig(n_local=n_local, local_size=local_size, p_jitter=1.0, p_gray=0.3,
+                                p_blur=[0.5] * (2 + n_local), p_solarize=[0.5] * (2 + n_local))
+    worst, frac = _check_against_torchvision(pf, scene, cfg)
+    assert frac < 1e-3, frac
+
+
+def test_f32_and_bf16_outputs_agree_with_u8(pf, scene):
+    """The normalised outputs of a config without blur are exactly the u8 crops through the LUT."""
+    torch = pytest.importorskip("torch")
+    ss, specs, _ = scene
+    cfg = pf.mc.MultiCropConfig(p_blur=[0.0] * 10)
+    g8, l8, _ = _run(pf, ss, specs, cfg, "u8", seed=9)
+    gf, lf, _ = _run(pf, ss, specs, cfg, "f32", seed=9)
+    mean = np.asarray(pf.IMAGENET_MEAN, np.float32)[:, None, None]
+    std = np.asarray(pf.IMAGENET_STD, np.float32)[:, None, None]
+    for u8, f32 in ((g8, gf), (l8, lf)):
+        want = (u8.cpu().numpy().astype(np.float32) / np.float32(255.0) - mean) / std
+        assert np.array_equal(f32.cpu().numpy(), want)
