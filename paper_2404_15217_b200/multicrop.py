@@ -185,7 +185,9 @@ class MultiCropLoader:
         S = self.mc.src_size
         self.specs_slots = [torch.empty((batch_size, 64), dtype=torch.uint8, device="cuda") for _ in range(2)]
         self.prefetch = prefetch
-        self._side = torch.cuda.Stream()
+        # high priority: the next step's sampler blocks are scheduled ahead of this step's
+        # multi-crop blocks as SMs free up, so the prefetch finishes inside the step
+        self._side = torch.cuda.Stream(priority=-1)
         self._ready = [None, None]
         self._free = [torch.cuda.Event(), torch.cuda.Event()]
         self._next_slot = 0

@@ -202,7 +202,7 @@ class RegionLoader:
         self.dtype, self.layout, self.mean, self.std = dtype, layout, mean, std
         self.prefetch = prefetch
         self.specs_slots = [torch.empty((batch_size, 64), dtype=torch.uint8, device="cuda") for _ in range(2)]
-        self._side = torch.cuda.Stream()
+        self._side = torch.cuda.Stream(priority=-1)  # sampler prefetch ahead of the reads (see MultiCropLoader)
         self._ready = [None, None]
         self._free = [torch.cuda.Event(), torch.cuda.Event()]
         self._next = 0
