@@ -39,7 +39,8 @@ enum pf_status {
     PF_ERR_CUDA = 6,             /* CUDA runtime failure */
     PF_ERR_EMPTY_FOREGROUND = 7, /* foreground.EmptyForegroundError (pkg/foreground.py:33) */
     PF_ERR_CAPACITY = 8,         /* caller buffer too small; required sizes were written */
-    PF_ERR_INTERNAL = 9
+    PF_ERR_INTERNAL = 9,
+    PF_ERR_DECODE = 10           /* store.DecodeError (pkg/store.py:62) */
 };
 
 /* Output element types for the normalising epilogues. */
@@ -245,6 +246,32 @@ int pf_png_inflate(const uint8_t* zdata_dev, const int64_t* zoff_dev, int32_t n,
 int pf_png_unfilter(const uint8_t* raw_dev, const int64_t* roff_dev, const int32_t* tile_w_dev,
                     const int32_t* tile_h_dev, uint8_t* const* dst_dev, int32_t tile_size, int32_t n,
                     int32_t* status_dev, void* stream);
+
+/* On-GPU baseline JPEG tile decode (decode_tile's Pillow path for JPEG stores,
+ * pkg/store.py:397-426), bit-exact with libjpeg-turbo's default decompression
+ * (accurate integer IDCT, fancy 2x2 chroma upsampling).  tiles_dev: n packed
+ * tile records (layout in csrc/pf_jpeg.cu, sizes via pf_jpeg_struct_sizes);
+ * data_dev: unstuffed entropy-coded segments; huff_dev / quant_dev: table
+ * pools; coef_dev / planes_dev: scratch; blk_*: the (tile, component, block)
+ * list for the IDCT; px_off_dev: exclusive prefix of tile pixel counts.
+ * status_dev[t] = 0 or a negative entropy-decode error. */
+int pf_jpeg_decode(const void* tiles_dev, int32_t n, const uint8_t* data_dev, const void* huff_dev,
+                   const uint16_t* quant_dev, int16_t* coef_dev, uint8_t* planes_dev, const int32_t* blk_tile_dev,
+                   const int32_t* blk_comp_dev, const int32_t* blk_index_dev, int32_t nblk,
+                   const int64_t* px_off_dev, int64_t total_px, int32_t tile_size, int32_t* status_dev,
+                   void* stream);
+int32_t pf_jpeg_struct_sizes(int32_t* huff, int32_t* tile);
+
+/* Host preparation for pf_jpeg_decode: parse n JPEG files bytes[off[t] .. off[t+1])
+ * of expected size tw[t] x th[t] into tile records (destination slot dst[t]),
+ * de-duplicated Huffman / quant pools, unstuffed entropy segments and the IDCT
+ * block list (buffer bounds in csrc/pf_jpeg_host.cpp).  ok_out[t] = 1 marks a
+ * tile the GPU path does not take (progressive, restart markers, other chroma
+ * sampling) for the host decoder; malformed tiles fail with PF_ERR_DECODE. */
+int pf_jpeg_prepare(const uint8_t* bytes, const int64_t* off, const int32_t* tw, const int32_t* th,
+                    const uint64_t* dst, int32_t n, void* tiles_out, int32_t* ok_out, uint8_t* data_out,
+                    void* huff_out, uint16_t* quant_out, int32_t* blk_tile_out, int32_t* blk_comp_out,
+                    int32_t* blk_index_out, int64_t* px_off_out, int64_t* counts_out);
 
 /* Capped replay draws (replaces CappedCache.draw inside capped_stream,
  * pkg/sampler.py:230-281): out[i] = stored[randrange(n_stored)] with the

@@ -30,6 +30,7 @@ PF_ERR_CUDA = 6
 PF_ERR_EMPTY_FOREGROUND = 7
 PF_ERR_CAPACITY = 8
 PF_ERR_INTERNAL = 9
+PF_ERR_DECODE = 10
 
 PF_U8, PF_F32, PF_BF16 = 0, 1, 2
 PF_HWC, PF_NCHW = 0, 1
@@ -196,6 +197,9 @@ class _Lib:
             ),
             "pf_capped_draw": ([u64, vp, vp, i32, i32, vp, vp], C.c_int),
             "pf_png_inflate": ([vp, vp, i32, vp, vp, vp, vp, vp], C.c_int),
+            "pf_jpeg_decode": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, i64, i32, vp, vp], C.c_int),
+            "pf_jpeg_struct_sizes": ([C.POINTER(i32), C.POINTER(i32)], C.c_int32),
+            "pf_jpeg_prepare": ([vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
             "pf_png_unfilter": ([vp, vp, vp, vp, vp, i32, i32, vp, vp], C.c_int),
             "pf_crop_params": ([u64, i32, u64, i32, C.POINTER(MultiCropConfig), vp, vp], C.c_int),
             "pf_multicrop": (
@@ -248,6 +252,7 @@ def status_error(rc: int, msg: str) -> Exception:
         PF_ERR_NO_SAMPLABLE: errors.NoSamplableSlideError,
         PF_ERR_EMPTY_FOREGROUND: errors.EmptyForegroundError,
         PF_ERR_CAPACITY: errors.CapacityError,
+        PF_ERR_DECODE: errors.DecodeError,
     }.get(rc, errors.NativeError)(msg)
 
 

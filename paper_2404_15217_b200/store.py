@@ -267,7 +267,7 @@ class GpuSlide:
         for li, lv in enumerate(rec.levels):
             nx, ny = rec.tile_grid(li)
             host = np.zeros((ny, nx, T, T, 3), dtype=np.uint8)
-            png = []  # (tx, ty, tw, th, zlib stream) decoded on the GPU
+            png, jpg = [], []  # (tx, ty, tw, th, zlib stream | JPEG file) decoded on the GPU
             for ty in range(ny):
                 for tx in range(nx):
                     loc = rec.chunks.get((li, tx, ty))
@@ -279,10 +279,18 @@ class GpuSlide:
                         if z is not None:
                             png.append((tx, ty, tw, th, z))
                             continue
+                    if gpu_png and loc["codec"] == "jpeg":
+                        jpg.append((tx, ty, tw, th, _read_chunk_bytes(root, loc)))
+                        continue
                     host[ty, tx, :th, :tw] = _read_chunk(root, loc, tw, th)
             dev = torch.from_numpy(host).cuda()
             if png:
                 _decode_png_tiles(dev, T, png, stream)
+            if jpg:
+                for k in _decode_jpeg_tiles(dev, T, jpg, stream):  # variants the GPU path does not take
+                    tx, ty, tw, th, _ = jpg[k]
+                    host_tile = _read_chunk(root, rec.chunks[(li, tx, ty)], tw, th)
+                    dev[ty, tx, :th, :tw] = torch.from_numpy(np.ascontiguousarray(host_tile)).cuda()
             levels.append(dev)
         return cls(rec, levels, factor)
 
@@ -441,6 +449,60 @@ def _decode_png_tiles(level, T: int, tiles, stream=None, chunk: int = 4096) -> N
         if len(bad):
             t = part[int(bad[0])]
             raise DecodeError(f"cannot decode png tile ({t[0]}, {t[1]}): inflate/unfilter status {int(st[bad[0]])}")
+
+
+_JPEG_TILE_BYTES, _JPEG_HUFF_BYTES = 184, 1420  # sizeof(JpegTile), sizeof(JpegHuff) (csrc/pf_jpeg.h)
+
+
+def _decode_jpeg_tiles(level, T: int, tiles, stream=None) -> list:
+    """Decode JPEG tiles (tx, ty, tw, th, file bytes) on the GPU into a dense level
+    [ty, tx, T, T, 3]: native host preparation (pf_jpeg_prepare) + pf_jpeg_decode.  Returns the
+    indices of tiles the GPU path does not take (progressive, restart markers, other chroma
+    sampling), which the caller decodes on the host."""
+    torch = N.require_cuda()
+    L = N.lib()
+    n = len(tiles)
+    if n == 0:
+        return []
+    nx = level.shape[1]
+    tb = T * T * 3
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum([len(t[4]) for t in tiles])
+    data = np.frombuffer(b"".join(t[4] for t in tiles), np.uint8)
+    tw = np.array([t[2] for t in tiles], np.int32)
+    th = np.array([t[3] for t in tiles], np.int32)
+    dst = np.array([int(level.data_ptr()) + (t[1] * nx + t[0]) * tb for t in tiles], np.uint64)
+    max_blk = int(np.sum(((tw.astype(np.int64) + 7) // 8) * ((th.astype(np.int64) + 7) // 8) * 3))
+    rec = np.zeros(n * _JPEG_TILE_BYTES, np.uint8)
+    ok = np.zeros(n, np.int32)
+    pool = np.zeros(len(data) + 8, np.uint8)
+    huff = np.zeros(4 * n * _JPEG_HUFF_BYTES, np.uint8)
+    quant = np.zeros(4 * n * 64, np.uint16)
+    bt, bc, bi = (np.zeros(max(max_blk, 1), np.int32) for _ in range(3))
+    px = np.zeros(n, np.int64)
+    counts = np.zeros(7, np.int64)
+    p = lambda a: a.ctypes.data  # noqa: E731
+    N.check(L.pf_jpeg_prepare(p(data), p(off), p(tw), p(th), p(dst), n, p(rec), p(ok), p(pool), p(huff), p(quant),
+                              p(bt), p(bc), p(bi), p(px), p(counts)), "pf_jpeg_prepare")
+    nh, nq, nblk, ndata, ncoef, nplane, npx = (int(v) for v in counts)
+    if nblk:
+        dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", non_blocking=False)  # noqa: E731
+        rec_d, pool_d = dv(rec), dv(pool[:ndata + 8])
+        huff_d, quant_d = dv(huff[:nh * _JPEG_HUFF_BYTES]), dv(quant[:nq * 64])
+        bt_d, bc_d, bi_d, px_d = dv(bt[:nblk]), dv(bc[:nblk]), dv(bi[:nblk]), dv(px)
+        coef = torch.empty(ncoef, dtype=torch.int16, device="cuda")
+        planes = torch.empty(nplane, dtype=torch.uint8, device="cuda")
+        status = torch.from_numpy(ok.copy()).cuda()  # host-path tiles are skipped by the kernels
+        N.check(L.pf_jpeg_decode(rec_d.data_ptr(), n, pool_d.data_ptr(), huff_d.data_ptr(), quant_d.data_ptr(),
+                                 coef.data_ptr(), planes.data_ptr(), bt_d.data_ptr(), bc_d.data_ptr(), bi_d.data_ptr(),
+                                 nblk, px_d.data_ptr(), npx, T, status.data_ptr(), N.stream_ptr(stream)),
+                "pf_jpeg_decode")
+        st = status.cpu().numpy()
+        bad = np.flatnonzero((st != 0) & (ok == 0))
+        if len(bad):
+            t = tiles[int(bad[0])]
+            raise DecodeError(f"cannot decode jpeg tile ({t[0]}, {t[1]}): entropy status {int(st[bad[0]])}")
+    return [int(i) for i in np.flatnonzero(ok)]
 
 
 def _read_chunk(root: Path, loc: dict, tw: int, th: int) -> np.ndarray:
