@@ -260,7 +260,7 @@ int pf_jpeg_decode(const void* tiles_dev, int32_t n, const uint8_t* data_dev, co
                    const int32_t* blk_comp_dev, const int32_t* blk_index_dev, int32_t nblk,
                    const int64_t* px_off_dev, int64_t total_px, int32_t tile_size, int32_t* status_dev,
                    void* stream);
-int32_t pf_jpeg_struct_sizes(int32_t* huff, int32_t* tile);
+int pf_jpeg_struct_sizes(int32_t* huff, int32_t* tile);
 
 /* Host preparation for pf_jpeg_decode: parse n JPEG files bytes[off[t] .. off[t+1])
  * of expected size tw[t] x th[t] into tile records (destination slot dst[t]),

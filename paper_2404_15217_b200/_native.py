@@ -198,7 +198,7 @@ class _Lib:
             "pf_capped_draw": ([u64, vp, vp, i32, i32, vp, vp], C.c_int),
             "pf_png_inflate": ([vp, vp, i32, vp, vp, vp, vp, vp], C.c_int),
             "pf_jpeg_decode": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, i64, i32, vp, vp], C.c_int),
-            "pf_jpeg_struct_sizes": ([C.POINTER(i32), C.POINTER(i32)], C.c_int32),
+            "pf_jpeg_struct_sizes": ([C.POINTER(i32), C.POINTER(i32)], C.c_int),
             "pf_jpeg_prepare": ([vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
             "pf_png_unfilter": ([vp, vp, vp, vp, vp, i32, i32, vp, vp], C.c_int),
             "pf_crop_params": ([u64, i32, u64, i32, C.POINTER(MultiCropConfig), vp, vp], C.c_int),

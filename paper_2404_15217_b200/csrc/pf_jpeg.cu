@@ -268,7 +268,7 @@ extern "C" int pf_jpeg_decode(const void* tiles_dev, int32_t n, const uint8_t* d
     return rc;
 }
 
-extern "C" int32_t pf_jpeg_struct_sizes(int32_t* huff, int32_t* tile) {
+extern "C" int pf_jpeg_struct_sizes(int32_t* huff, int32_t* tile) {
     if (!huff || !tile) return fail(PF_ERR_INVALID_ARG, "pf_jpeg_struct_sizes: bad arguments");
     *huff = (int32_t)sizeof(JpegHuff);
     *tile = (int32_t)sizeof(JpegTile);

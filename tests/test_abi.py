@@ -159,3 +159,52 @@ def test_argument_validation_without_device(native):
     assert L.pf_read_regions(8, 8, 0, 224, 0, 0, None, None, 8, None) == native.PF_OK
     assert L.pf_read_regions(8, 8, 1, 600, 0, 0, None, None, 8, None) == native.PF_ERR_INVALID_ARG
     assert L.pf_rrc_table_build(224, 32, 8, None) == native.PF_ERR_INVALID_ARG  # down-ratio > 3.5
+
+
+def test_jpeg_record_sizes_match_host_layout(native):
+    """The packed JPEG records the host preparation writes have the device structs' sizes."""
+    from paper_2404_15217_b200 import store
+
+    h, t = C.c_int32(), C.c_int32()
+    assert native.lib().pf_jpeg_struct_sizes(C.byref(h), C.byref(t)) == native.PF_OK
+    assert (h.value, t.value) == (store._JPEG_HUFF_BYTES, store._JPEG_TILE_BYTES)
+
+
+def test_jpeg_prepare_on_host(native):
+    """pf_jpeg_prepare parses Pillow's baseline files on the CPU: one Huffman/quant pool entry per
+    distinct table, the 4:2:0 block list, and host fallback for progressive files."""
+    import io
+
+    import numpy as np
+    from PIL import Image
+
+    from paper_2404_15217_b200 import store
+
+    rs = np.random.default_rng(0)
+    files = []
+    for prog in (False, False, True):
+        buf = io.BytesIO()
+        Image.fromarray(rs.integers(0, 256, (24, 40, 3), dtype=np.uint8)).save(buf, format="JPEG", quality=90,
+                                                                                 progressive=prog)
+        files.append(buf.getvalue())
+    n = len(files)
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum([len(f) for f in files])
+    data = np.frombuffer(b"".join(files), np.uint8)
+    tw, th = np.full(n, 40, np.int32), np.full(n, 24, np.int32)
+    dst = np.zeros(n, np.uint64)
+    rec = np.zeros(n * store._JPEG_TILE_BYTES, np.uint8)
+    ok = np.zeros(n, np.int32)
+    pool = np.zeros(len(data) + 8, np.uint8)
+    huff = np.zeros(4 * n * store._JPEG_HUFF_BYTES, np.uint8)
+    quant = np.zeros(4 * n * 64, np.uint16)
+    blk = [np.zeros(n * 5 * 3 * 3, np.int32) for _ in range(3)]
+    px, counts = np.zeros(n, np.int64), np.zeros(7, np.int64)
+    p = lambda a: a.ctypes.data  # noqa: E731
+    rc = native.lib().pf_jpeg_prepare(p(data), p(off), p(tw), p(th), p(dst), n, p(rec), p(ok), p(pool), p(huff),
+                                      p(quant), p(blk[0]), p(blk[1]), p(blk[2]), p(px), p(counts))
+    assert rc == native.PF_OK
+    assert ok.tolist() == [0, 0, 1]
+    n_huff, n_quant, n_blocks = counts[:3]
+    assert (n_huff, n_quant) == (4, 2)  # DC/AC x luma/chroma, shared by both baseline files
+    assert n_blocks == 2 * (2 * 3 * 4 + 2 * 3 * 2)  # per file: 3x2 MCUs of 4 Y + Cb + Cr blocks
