@@ -19,7 +19,6 @@
 // a window that ran out) the walk continues on the sequential exact path.
 #include <algorithm>
 
-#include <stdlib.h>
 
 #include "pf_common.cuh"
 #include "pf_poly.cuh"
@@ -483,10 +482,7 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     if (rc) return rc;
     // small blocks: most candidates finish in the whole-window shortcut, and a boundary window's
     // warp must not pin idle warps' shared memory (measured: 8-warp blocks ran at 15 % occupancy)
-    static const int warps = [] {
-        const char* v = getenv("PF_EVAL_WARPS");  // tuning experiments only
-        return v ? atoi(v) : 2;
-    }();
+    const int warps = 2;
     const size_t eval_smem = (size_t)warps * overlap_smem_bytes(cfg->grid);
     const size_t bm_bytes_all = (size_t)cfg->n_slides * (window / 32) * 4;
     const int bm_in_smem = rounds > 0 && bm_bytes_all <= 160 * 1024;
