@@ -106,7 +106,7 @@ __device__ __forceinline__ void emit_spec(const pf_sampler_config& cfg, const pf
 // ---------------------------------------------------------------------------
 // Speculative evaluation: one warp per (slide, window offset).
 // ---------------------------------------------------------------------------
-__global__ void sample_eval_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
+__global__ void __launch_bounds__(64, 16) sample_eval_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
                                    const pf_sampler_state* state, SamplerWs ws, int window, int n) {
     extern __shared__ __align__(16) uint32_t s_masks[];
     if (state->status != PF_OK || state->emitted >= n) return;
