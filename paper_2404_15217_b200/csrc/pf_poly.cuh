@@ -248,22 +248,34 @@ __device__ inline int warp_overlap_count(const PolyView& P, double x, double y, 
 
 // Smallest covered-cell count c with c / grid^2 >= min_fg in the reference's FP64 arithmetic
 // (the division it performs, so the comparison is exact); grid^2 + 1 if none.
-__device__ inline int accept_cells(int grid, double min_fg) {
+// Host and device agree: both divide in IEEE binary64 round-to-nearest.
+__host__ __device__ inline int accept_cells(int grid, double min_fg) {
+#ifdef __CUDA_ARCH__
+#define PF_DDIV(a, b) __ddiv_rn((a), (b))
+#else
+#define PF_DDIV(a, b) ((a) / (b))
+#endif
     const double g2 = (double)grid * (double)grid;
     int c = (int)fmax(0.0, fmin(g2, ceil(min_fg * g2)));
-    while (c > 0 && __ddiv_rn((double)(c - 1), g2) >= min_fg) --c;
-    while (c <= (int)g2 && !(__ddiv_rn((double)c, g2) >= min_fg)) ++c;
+    while (c > 0 && PF_DDIV((double)(c - 1), g2) >= min_fg) --c;
+    while (c <= (int)g2 && !(PF_DDIV((double)c, g2) >= min_fg)) ++c;
+#undef PF_DDIV
     return c;
 }
 
 // overlap_fraction(rect) >= min_fg, decided without finishing the lattice when the covered
 // cells so far already reach the threshold, or the rows left cannot (the sampler only needs
 // the acceptance bit, pkg/sampler.py:174-179).  All lanes return the same value.
+// `need` = accept_cells(grid, min_fg), hoisted out of the per-candidate path by the caller.
 __device__ inline bool warp_overlap_accept(const PolyView& P, double x, double y, double w, double h, int grid,
-                                           uint32_t* smem, double min_fg) {
-    const int need = accept_cells(grid, min_fg);
+                                           uint32_t* smem, double min_fg, int need) {
     const int c = warp_overlap_count_upto(P, x, y, w, h, grid, smem, need);
     return c < 0 ? 0.0 >= min_fg : c >= need;  // c < 0: bbox early-out, fraction 0.0
+}
+
+__device__ inline bool warp_overlap_accept(const PolyView& P, double x, double y, double w, double h, int grid,
+                                           uint32_t* smem, double min_fg) {
+    return warp_overlap_accept(P, x, y, w, h, grid, smem, min_fg, accept_cells(grid, min_fg));
 }
 
 }  // namespace pf

@@ -69,9 +69,7 @@ __host__ __device__ inline int64_t ws_bytes(int n_slides, int window) {
 }
 
 // RandomStream.weighted_index (rng.py:88-103) given the stream draw u.
-__device__ __forceinline__ int weighted_pick(uint64_t u, const double* w, int n) {
-    double total = 0.0;
-    for (int i = 0; i < n; ++i) total = __dadd_rn(total, w[i]);
+__device__ __forceinline__ int weighted_pick(uint64_t u, const double* w, int n, double total) {
     const double v = __dadd_rn(0.0, __dmul_rn(u64_to_unit(u), __dsub_rn(total, 0.0)));
     double acc = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -80,6 +78,24 @@ __device__ __forceinline__ int weighted_pick(uint64_t u, const double* w, int n)
     }
     return n - 1;
 }
+
+// The reference sums the weights on every call (rng.py:95); the sum is the same each time,
+// so per-candidate callers take it precomputed (host sum in the same order, IEEE binary64).
+__host__ __device__ inline double weight_total(const double* w, int n) {
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) total = total + w[i];
+    return total;
+}
+
+__device__ __forceinline__ int weighted_pick(uint64_t u, const double* w, int n) {
+    return weighted_pick(u, w, n, weight_total(w, n));
+}
+
+// Per-launch constants of the speculative evaluation, computed once on the host.
+struct EvalConsts {
+    double weight_total;  // sum of cfg.mpp_weight
+    int32_t need;         // accept_cells(cfg.grid, cfg.min_foreground)
+};
 
 __device__ __forceinline__ void emit_spec(const pf_sampler_config& cfg, const pf_sampler_slide& sl,
                                           const pf_slide_desc& sd, int s, int x, int y, int mi,
@@ -107,17 +123,19 @@ __device__ __forceinline__ void emit_spec(const pf_sampler_config& cfg, const pf
 // Speculative evaluation: one warp per (slide, window offset).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(64, 16) sample_eval_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
-                                   const pf_sampler_state* state, SamplerWs ws, int window, int n) {
+                                   const pf_sampler_state* state, SamplerWs ws, int window, int n,
+                                   EvalConsts k) {
     extern __shared__ __align__(16) uint32_t s_masks[];
     if (state->status != PF_OK || state->emitted >= n) return;
     const int warp_in_block = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_in_block;
-    if (q >= (int64_t)cfg.n_slides * window) return;
-    const int s = (int)(q / window), a = (int)(q % window);
+    const uint32_t q = blockIdx.x * (blockDim.x >> 5) + warp_in_block;  // n_slides * window < 2^31 (host)
+    if (q >= (uint32_t)cfg.n_slides * (uint32_t)window) return;
+    const int s = (int)(q / (uint32_t)window), a = (int)(q % (uint32_t)window);
     const pf_sampler_slide& sl = slides[s];
     const uint64_t m0 = state->c_mpp, c0 = state->c_coords;
-    const int mi = weighted_pick(stream_u64(cfg.key_mpp, m0 + (uint64_t)a + 1), cfg.mpp_weight, cfg.n_mpps);
+    const int mi = weighted_pick(stream_u64(cfg.key_mpp, m0 + (uint64_t)a + 1), cfg.mpp_weight, cfg.n_mpps,
+                                 k.weight_total);
     const int fp = sl.fp[mi];
     const uint64_t nx = (uint64_t)(sl.x_hi[mi] - sl.x_lo[mi] + 1);
     const uint64_t ny = (uint64_t)(sl.y_hi[mi] - sl.y_lo[mi] + 1);
@@ -133,7 +151,7 @@ __global__ void __launch_bounds__(64, 16) sample_eval_kernel(pf_sampler_config c
     const PolyView P = poly_view(reinterpret_cast<const void*>(sl.poly_blob));
     uint32_t* sm = s_masks + warp_in_block * (overlap_smem_bytes(cfg.grid) / 4);
     const bool accept = warp_overlap_accept(P, (double)x, (double)y, (double)fp, (double)fp, cfg.grid, sm,
-                                            cfg.min_foreground);
+                                            cfg.min_foreground, k.need);
     if (lane == 0) {
         ws.cands[(size_t)s * window + a] = make_int4(x, y, mi, 0);
         if (accept)
@@ -472,7 +490,7 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
         cfg->max_attempts < 1)
         return fail(PF_ERR_INVALID_ARG, "pf_sample: bad config");
     if (n == 0) return PF_OK;
-    if (window < 32 || window % 32 != 0) rounds = 0;
+    if (window < 32 || window % 32 != 0 || (int64_t)cfg->n_slides * window >= (int64_t)1 << 31) rounds = 0;
     if (rounds > 0 && (!workspace || workspace_bytes < ws_bytes(cfg->n_slides, window)))
         return fail(PF_ERR_INVALID_ARG, "pf_sample: workspace too small");
     if (!all_fit) rounds = 0;
@@ -495,6 +513,9 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     if (rc) return rc;
     SamplerWs ws{};
     if (rounds > 0) ws = carve_ws(workspace, cfg->n_slides, window);
+    EvalConsts consts{};
+    consts.weight_total = weight_total(cfg->mpp_weight, cfg->n_mpps);
+    consts.need = accept_cells(cfg->grid, cfg->min_foreground);
     for (int r = 0; r < rounds; ++r) {
         const size_t bm_bytes = (size_t)cfg->n_slides * (window / 32) * 4;
         rc = check_cuda(cudaMemsetAsync(ws.bitmaps, 0, bm_bytes, st), "cudaMemsetAsync");
@@ -503,7 +524,8 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
         if (rc) return rc;
         const int64_t cands = (int64_t)cfg->n_slides * window;
         const int64_t blocks = (cands + warps - 1) / warps;
-        sample_eval_kernel<<<(unsigned)blocks, warps * 32, eval_smem, st>>>(*cfg, slides_dev, state_dev, ws, window, n);
+        sample_eval_kernel<<<(unsigned)blocks, warps * 32, eval_smem, st>>>(*cfg, slides_dev, state_dev, ws, window, n,
+                                                                             consts);
         if ((rc = after_launch("sample_eval_kernel"))) return rc;
         sample_walk_kernel<<<1, kWalkThreads, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws,
                                                                 window, n, 1, r == rounds - 1, bm_in_smem,
