@@ -14,7 +14,8 @@ import numpy as np
 
 from . import errors
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpfb200.so"
+# PF_B200_LIB: load another build of the same ABI (A/B timing of kernel variants)
+_LIB_PATH = Path(os.environ.get("PF_B200_LIB") or Path(__file__).resolve().parent / "_lib" / "libpfb200.so")
 
 PF_MAX_LEVELS = 12
 PF_MAX_MPPS = 8

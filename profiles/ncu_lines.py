@@ -28,5 +28,5 @@ for r in rows:
 tot_s = sum(a[0] for a in agg) or 1
 tot_i = sum(a[1] for a in agg) or 1
 print(f"total samples {tot_s}, warp-instructions {tot_i}")
-for s, i, f, ln, src in sorted(agg, reverse=True)[:top]:
+for s, i, f, ln, src in sorted(agg, key=lambda a: (a[0], a[1]), reverse=True)[:top]:
     print(f"{100*s/tot_s:5.1f}% smp {100*i/tot_i:5.1f}% inst  {f}:{ln}  {src}")
