@@ -7,6 +7,9 @@ where the oracle finishes in seconds, size-independent properties everywhere els
   traced polygons (FP64 lattice at coordinates up to 40000); the stream does not depend on
   how it is split into batches; every spec of a 1024 batch meets min_foreground on the
   device and, for a sample, in the oracle;
+* read_region (configs 1 and 3): sampled specs of a mixed-mpp batch (0.25 mpp passthrough,
+  0.5 mpp PIL-bilinear resample) against port.read_region on the device's level-0 pixels,
+  u8 bit-exact and the normalised f32 bit-exact;
 * multi-crop: sampled patches of a 1024-patch batch against torchvision on the raw level-0
   window (<= 1 LSB, the small-size bar); the batch split and a repeated launch give
   bit-identical crops (checksum of per-patch checksums).
@@ -127,6 +130,30 @@ def test_full_size_stream_is_batch_split_invariant_and_admissible(pf, c2, chunke
         assert np.all(fr >= 0.40)
         for r, f in zip(rects[:2], fr[:2]):  # the oracle on a sample: same FP64 fraction
             assert port.overlap_fraction(poly.rings, tuple(r), 128) == f
+
+
+def test_full_size_read_regions_mixed_mpp(pf, c2):
+    ss = pf.SlideSet([s for s, _ in c2])
+    cfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=[(0.25, 1.0), (0.5, 1.0)], seed=SEED)
+    smp = pf.GpuSampler(cfg, c2, slide_set=ss)
+    specs = smp.next_batch(256)
+    mean, std = pf.IMAGENET_MEAN, pf.IMAGENET_STD
+    u8 = ss.read_regions(specs, 224).cpu().numpy()
+    f32 = ss.read_regions(specs, 224, dtype="f32", mean=mean, std=std).cpu().numpy()
+    hs = smp.to_patch_specs(specs)
+    slides = {s.record.slide_id: s for s, _ in c2}
+    picked = [i for i in range(256) if hs[i].target_mpp == 0.25][:4] + [i for i in range(256) if hs[i].target_mpp == 0.5][:4]
+    assert len(picked) == 8
+    for i in picked:
+        sp = hs[i]
+        s = slides[sp.slide_id]
+        x0, y0 = max(0, sp.x - 2), max(0, sp.y - 2)
+        crop = _region(s, 0, x0, y0, min(W, sp.x + sp.width + 2) - x0, min(H, sp.y + sp.height + 2) - y0)
+        mpps = [lv.mpp for lv in s.record.levels]
+        want = port.read_region([crop], mpps, [1.0] * len(mpps), (sp.x - x0, sp.y - y0, sp.width, sp.height),
+                                sp.target_mpp, 224)
+        assert np.array_equal(u8[i], want), (i, sp)
+        assert np.array_equal(f32[i], port.normalize_patch(want, mean, std))
 
 
 @pytest.fixture(scope="module")
