@@ -211,3 +211,33 @@ def test_full_batch_split_and_repeat_are_bit_identical(pf, batch):
         parts.append(_checksums(torch, ga, la))
     assert torch.equal(torch.cat(parts), ref)
     assert torch.equal(g2, g) and torch.equal(l2, l)
+
+
+def test_config4_size_slide_compacted_matches_dense(pf):
+    """BASELINE configs[3] (residency): a 70000 x 55000 slide (the C4 mean size) compacted to its
+    reachable tiles serves a 1024-spec batch with the dense pyramid's bytes (crops and regions)."""
+    torch = pytest.importorskip("torch")
+    from paper_2404_15217_b200 import residency as R
+    from paper_2404_15217_b200.synthetic import synthetic_slide
+
+    s = synthetic_slide("c4", 70000, 55000, seed=4, downsample_factor=4)
+    thumb, scale = s.thumbnail_device(32)
+    bm = pf.BinaryMask(pf.foreground.mask_device(thumb, 1, 0.07, 1).cpu().numpy().astype(bool), scale)
+    poly = pf.polygon_from_mask(bm, slide_id="c4")
+    mpps = [(0.25, 1.0), (0.5, 1.0)]
+    cfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=mpps, seed=SEED)
+    ss = pf.SlideSet([s])
+    specs = pf.GpuSampler(cfg, [(s, poly)], slide_set=ss).next_batch(1024)
+    mc = pf.mc.MultiCropConfig()
+    params = pf.mc.crop_params(mc, 1024, seed=4)
+    src = ss.read_regions(specs, 224)
+    g0, l0 = pf.mc.multicrop(ss, specs, params, mc, dtype="bf16", src_hwc=src)
+    plan = R.reachable_tiles(s.record, bm.bits, scale, R.max_footprint(s.record, 224, mpps))
+    dense = R.dense_bytes(s.record)
+    s.compact(plan)
+    torch.cuda.empty_cache()
+    assert R.resident_bytes(s.record, plan) < 0.9 * dense
+    ss2 = pf.SlideSet([s])
+    src2 = ss2.read_regions(specs, 224)
+    g1, l1 = pf.mc.multicrop(ss2, specs, params, mc, dtype="bf16", src_hwc=src2)
+    assert torch.equal(src, src2) and torch.equal(g0, g1) and torch.equal(l0, l1)
