@@ -26,3 +26,11 @@ for name, mc in (("global", MultiCropConfig(n_local=0)), ("local", MultiCropConf
         multicrop(L.slide_set, specs, prm, mc, dtype="bf16")
     e.record(); torch.cuda.synchronize()
     print(f"{name}: {s.elapsed_time(e) / 20:.4f} ms")
+
+# bit-identity check across builds: sha256 of u8 crops (every op on, 1024 patches)
+import hashlib
+mc = MultiCropConfig(p_jitter=1.0, p_gray=0.2, p_blur=[0.5] * 10, p_solarize=[0.2] * 10)
+prm = crop_params(mc, 1024, seed=7, step=3)
+g, l = multicrop(L.slide_set, specs, prm, mc, dtype="u8")
+torch.cuda.synchronize()
+print("sha256", hashlib.sha256(g.cpu().numpy().tobytes() + l.cpu().numpy().tobytes()).hexdigest()[:16])
