@@ -206,6 +206,8 @@ class Feed:
 
 
 def make_feed(args, pf, plan, slides, rank, src_size=224, n_local=8, patch=224):
+    # speculation rounds per sampler call (the loaders' default, 2; PF_SAMPLER_ROUNDS for experiments)
+    rounds = int(os.environ.get("PF_SAMPLER_ROUNDS", "2"))
     from paper_2404_15217_b200.multicrop import MultiCropConfig, MultiCropLoader
     from paper_2404_15217_b200.pipeline import RegionLoader
 
@@ -222,7 +224,7 @@ def make_feed(args, pf, plan, slides, rank, src_size=224, n_local=8, patch=224):
         mpps = [(0.25 * patch / 224.0, 1.0)]
     scfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=mpps, seed=plan.sampler_seed)
     mc = MultiCropConfig(n_local=n_local)
-    loader = MultiCropLoader(slides, scfg, mc, batch_size=args.batch, rank=rank, dtype=args.dtype)
+    loader = MultiCropLoader(slides, scfg, mc, batch_size=args.batch, rank=rank, dtype=args.dtype, rounds=rounds)
     tag = {"2": "C2", "3": "C3 (mpp U{0.25,0.5,1,2})", "4": "C4", "5": f"C5 point (patch {patch}->224, L={n_local})"}[args.config]
     if args.config == "4":
         r = getattr(args, "residency", None) or {}

@@ -161,7 +161,7 @@ class MultiCropLoader:
     """
 
     def __init__(self, slides, sampler_config, mc_config: MultiCropConfig | None = None, *, batch_size: int = 1024,
-                 rank: int = 0, dtype: str = "bf16", mean=IMAGENET_MEAN, std=IMAGENET_STD, window=None, rounds: int = 4,
+                 rank: int = 0, dtype: str = "bf16", mean=IMAGENET_MEAN, std=IMAGENET_STD, window=None, rounds: int = 2,
                  prefetch: bool = True, cap: int | None = None):
         torch = N.require_cuda()
         from .sampler import CappedSampler, GpuSampler
