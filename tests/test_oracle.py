@@ -165,3 +165,17 @@ def test_capped_stream_oracle_and_host_vs_reference(goldens):
 
     with pytest.raises(ValueError):
         S.CappedCache(0)
+
+
+@pytest.mark.parametrize("out_size", [16, 96, 112, 224])
+def test_torch_aa_taps_never_need_the_uint8_clamp(out_size):
+    """The multi-crop kernel drops torch's [0, 255] clamp after each resample pass
+    (pf_multicrop.cu kNoClampNote): every output's int16 taps are >= 0 and
+    255 * sum(taps) + 2^(prec-1) < 2^(prec+8), for every crop extent the kernel accepts
+    (in <= 3.5 * out) of the 224-px source."""
+    for in_size in range(1, min(224, int(3.5 * out_size)) + 1):
+        _, q, p = port.aa_axis_table(in_size, out_size, "torch")
+        assert p >= 14
+        for taps in q:
+            assert min(taps, default=0) >= 0
+            assert 255 * sum(taps) + (1 << (p - 1)) < (1 << (p + 8)), (in_size, out_size)
