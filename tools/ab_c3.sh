@@ -1,0 +1,6 @@
+# A/B of bench config 3 (mixed mpp, PIL resample): in-tree build vs ab/*.so on the same box
+run() { python bench.py --config 3 --no-e2e --no-cpu-baseline "$@" 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print(d["value"], d["stages_ms"])'; }
+for r in 1 2; do
+  echo "tree $(run)"
+  for f in ab/*.so; do echo "$(basename $f) $(PF_B200_LIB=$PWD/$f run)"; done
+done
