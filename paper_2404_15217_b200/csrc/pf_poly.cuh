@@ -145,6 +145,10 @@ __host__ __device__ constexpr int overlap_words(int grid) { return (grid + 1 + 3
 __host__ __device__ constexpr int overlap_smem_bytes(int grid) {
     return (2 * grid + 1) * overlap_words(grid) * 4;
 }
+// ... when it only counts with a stop (rows traced in chunks of 32: warp_overlap_accept)
+__host__ __device__ constexpr int overlap_smem_bytes_chunked(int grid) {
+    return (2 * (grid < 32 ? grid : 32) + 1) * overlap_words(grid) * 4;
+}
 
 // Covered cells of lattice cell rows [r_lo, r_hi): corner rows r_lo..r_hi and centre rows
 // r_lo..r_hi-1 are traced into `smem`, then counted.  With stop >= 0 the rows are taken in

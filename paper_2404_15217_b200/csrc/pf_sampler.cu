@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(64, 16) sample_eval_kernel(pf_sampler_config c
     const int x = sl.x_lo[mi] + (int)(vx % nx);
     const int y = sl.y_lo[mi] + (int)(vy % ny);
     const PolyView P = poly_view(reinterpret_cast<const void*>(sl.poly_blob));
-    uint32_t* sm = s_masks + warp_in_block * (overlap_smem_bytes(cfg.grid) / 4);
+    uint32_t* sm = s_masks + warp_in_block * (overlap_smem_bytes_chunked(cfg.grid) / 4);
     const bool accept = warp_overlap_accept(P, (double)x, (double)y, (double)fp, (double)fp, cfg.grid, sm,
                                             cfg.min_foreground, k.need);
     if (lane == 0) {
@@ -501,7 +501,8 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     // small blocks: most candidates finish in the whole-window shortcut, and a boundary window's
     // warp must not pin idle warps' shared memory (measured: 8-warp blocks ran at 15 % occupancy)
     const int warps = 2;
-    const size_t eval_smem = (size_t)warps * overlap_smem_bytes(cfg->grid);
+    // chunked row masks (1.3 KB per warp at grid 128): an eval block fits beside a multi-crop CTA
+    const size_t eval_smem = (size_t)warps * overlap_smem_bytes_chunked(cfg->grid);
     const size_t bm_bytes_all = (size_t)cfg->n_slides * (window / 32) * 4;
     const int bm_in_smem = rounds > 0 && bm_bytes_all <= 160 * 1024;
     const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid), bm_in_smem ? bm_bytes_all : (size_t)0);
