@@ -213,7 +213,8 @@ def make_feed(args, pf, plan, slides, rank, src_size=224, n_local=8, patch=224):
 
     if args.config == "1":
         scfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=[(0.25, 1.0)], seed=plan.sampler_seed)
-        loader = RegionLoader(slides, scfg, batch_size=args.batch, dtype=args.dtype)
+        chunk = int(os.environ["PF_REGION_CHUNK"]) if os.environ.get("PF_REGION_CHUNK") else None  # experiment knob
+        loader = RegionLoader(slides, scfg, batch_size=args.batch, dtype=args.dtype, chunk=chunk)
         el = 4 if args.dtype == "f32" else 2
         bpp = 224 * 224 * 3 + 224 * 224 * 3 * el
         wl = (f"C1: {args.slides} slide {args.width}x{args.height} in HBM, sat>0.07+morph mask on 1/32 thumbnail, "

@@ -186,12 +186,14 @@ class RegionLoader:
 
     ``slides``: list of (GpuSlide, ForegroundPolygon).  Each ``next_batch`` returns a
     [batch, 3, S, S] tensor of (v/255 - mean)/std (``dtype`` f32/bf16) or raw uint8, for the
-    next ``batch`` specs of the reference epoch_stream.  The sampler for step k+1 runs on a
-    side stream while step k is read (``prefetch``).
+    next ``batch`` specs of the reference epoch_stream.  With ``prefetch`` the sampler runs on a
+    side stream, ``chunk`` batches per call (the stream does not depend on how it is split), one
+    chunk ahead of the reads: small batches amortise the sampler's fixed launch latency.
     """
 
     def __init__(self, slides, sampler_config, *, batch_size: int = 256, dtype: str = "f32", layout: str = "nchw",
-                 mean=IMAGENET_MEAN, std=IMAGENET_STD, prefetch: bool = True, window=None, rounds: int = 2):
+                 mean=IMAGENET_MEAN, std=IMAGENET_STD, prefetch: bool = True, window=None, rounds: int = 2,
+                 chunk: int | None = None):
         torch = N.require_cuda()
         from .sampler import GpuSampler
 
@@ -201,11 +203,14 @@ class RegionLoader:
         self.out_size = sampler_config.patch_size
         self.dtype, self.layout, self.mean, self.std = dtype, layout, mean, std
         self.prefetch = prefetch
-        self.specs_slots = [torch.empty((batch_size, 64), dtype=torch.uint8, device="cuda") for _ in range(2)]
+        self.chunk = max(1, chunk if chunk is not None else 8192 // max(1, batch_size)) if prefetch else 1
+        rows = batch_size * self.chunk
+        self.specs_slots = [torch.empty((rows, 64), dtype=torch.uint8, device="cuda") for _ in range(2)]
         self._side = torch.cuda.Stream(priority=-1)  # sampler prefetch ahead of the reads (see MultiCropLoader)
         self._ready = [None, None]
         self._free = [torch.cuda.Event(), torch.cuda.Event()]
         self._next = 0
+        self._pos = 0  # batches of the current slot already served
         S = self.out_size
         tdt = {"u8": torch.uint8, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
         shape = (batch_size, 3, S, S) if layout == "nchw" else (batch_size, S, S, 3)
@@ -224,27 +229,32 @@ class RegionLoader:
         n = self.batch_size
         mark("begin")
         if not self.prefetch:
-            cur = 0
+            cur, pos = 0, 0
             self.sampler.next_batch(n, out=self.specs_slots[0], stream=st)
             mark("sample")
         else:
-            cur = self._next
+            cur, pos = self._next, self._pos
+            rows = n * self.chunk
             if self._ready[cur] is None:
                 self._side.wait_stream(st)
-                self.sampler.next_batch(n, out=self.specs_slots[cur], stream=self._side)
+                self.sampler.next_batch(rows, out=self.specs_slots[cur], stream=self._side)
                 self._ready[cur] = torch.cuda.Event()
                 self._ready[cur].record(self._side)
             st.wait_event(self._ready[cur])
             mark("sample_wait")
-            nxt = 1 - cur
-            self._side.wait_event(self._free[nxt])
-            self.sampler.next_batch(n, out=self.specs_slots[nxt], stream=self._side)
-            self._ready[nxt] = torch.cuda.Event()
-            self._ready[nxt].record(self._side)
-            self._next = nxt
-        self.slide_set.read_regions(self.specs_slots[cur], self.out_size, dtype=self.dtype, layout=self.layout,
+            if pos == 0:  # starting this slot: sample the next chunk into the other one
+                nxt = 1 - cur
+                self._side.wait_event(self._free[nxt])
+                self.sampler.next_batch(rows, out=self.specs_slots[nxt], stream=self._side)
+                self._ready[nxt] = torch.cuda.Event()
+                self._ready[nxt].record(self._side)
+        specs = self.specs_slots[cur][pos * n:(pos + 1) * n]
+        self.slide_set.read_regions(specs, self.out_size, dtype=self.dtype, layout=self.layout,
                                     mean=self.mean, std=self.std, out=self.out, stream=st, planned=True)
         mark("read")
         if self.prefetch:
-            self._free[cur].record(st)
-        return {"patches": self.out, "specs": self.specs_slots[cur]}
+            self._pos = pos + 1
+            if self._pos == self.chunk:  # slot consumed: free it for the chunk after next
+                self._free[cur].record(st)
+                self._next, self._pos = 1 - cur, 0
+        return {"patches": self.out, "specs": specs}
