@@ -432,6 +432,7 @@ def result_line(feed, args, world, elapsed_ms, stage_ms, launches, clocks, st, e
             "traffic": traffic,
             "algorithmic_bytes_per_patch": feed.bytes_per_patch,
             "per_launch_ms": round(k_ms, 4),
+            "frac_of_nominal_8tbs": round(achieved / 8000.0, 4),  # north_star's ~8 TB/s nominal HBM3e
         },
         "issue_roofline": issue_roofline(args, k_ms),
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
