@@ -336,12 +336,18 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                 if (span > 0) {
                     const uint32_t* bm = bm_all + (size_t)w.cur_slide * words;
                     const int wfirst = a0 >> 5, wlast = (a0 + span - 1) >> 5;
-                    for (int base = wfirst; base <= wlast && found < 0; base += 32) {
+                    // common case first (acceptance ~0.5): the next accepted offset lies in a0's word
+                    uint32_t b0 = bm[wfirst] & (0xffffffffu << (a0 & 31));
+                    if (wfirst == wlast) {
+                        const int e = (a0 + span - 1) & 31;
+                        b0 &= (e == 31) ? 0xffffffffu : ((1u << (e + 1)) - 1u);
+                    }
+                    if (b0) found = wfirst * 32 + __ffs(b0) - 1;
+                    for (int base = wfirst + 1; base <= wlast && found < 0; base += 32) {
                         const int wi = base + lane;
                         uint32_t bits = 0;
                         if (wi <= wlast) {
                             bits = bm[wi];
-                            if (wi == wfirst) bits &= 0xffffffffu << (a0 & 31);
                             if (wi == wlast) {
                                 const int e = (a0 + span - 1) & 31;
                                 bits &= (e == 31) ? 0xffffffffu : ((1u << (e + 1)) - 1u);

@@ -1,3 +1,3 @@
-# config-1 throughput by sampler prefetch chunk (PF_REGION_CHUNK; default 1024 // batch)
+# config-1 throughput (sampler-walk bound): in-tree build vs ab/*.so
 run() { python bench.py --config 1 --steps 300 --no-e2e --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print(d["value"], d["stages_ms"])'; }
-for c in 4 8 16 32; do echo "chunk=$c $(PF_REGION_CHUNK=$c run)"; done
+for r in 1 2; do echo "tree $(run)"; for f in ab/*.so; do echo "$(basename $f) $(PF_B200_LIB=$PWD/$f run)"; done; done
