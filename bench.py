@@ -490,7 +490,7 @@ def run_sweep(args, pf, plan, slides, rank, world, local, torch, dist, N):
             for n_local in (0, 4, 8):
                 for dtype in ("bf16", "f32"):
                     a = argparse.Namespace(**vars(args))
-                    a.batch, a.dtype, a.steps, a.warmup = batch, dtype, max(2, min(args.steps, 5)), 2
+                    a.batch, a.dtype, a.steps, a.warmup = batch, dtype, max(3, min(args.steps, 5)), 3
                     feed = make_feed(a, pf, plan, slides, rank, n_local=n_local, patch=patch)
                     elapsed_ms, stage_ms, launches, clocks = timed_run(feed, a, torch, dist, world, local, N)
                     st = feed.sampler.check()
