@@ -17,7 +17,6 @@ import json
 from dataclasses import dataclass, field
 from pathlib import Path
 
-import numpy as np
 
 from . import _native as N
 from . import rng
