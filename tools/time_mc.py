@@ -3,11 +3,11 @@
 usage: python tools/time_mc.py   (PF_B200_LIB selects another build of the library)
 """
 import sys; sys.path.insert(0, '.')
-import argparse, torch
+import argparse, os, torch
 import bench
 from paper_2404_15217_b200.multicrop import MultiCropConfig, MultiCropLoader, crop_params, multicrop
 
-args = argparse.Namespace(config="2", batch=1024, slides=4, width=40000, height=30000, dtype="bf16", gpus=1)
+args = argparse.Namespace(config="2", batch=1024, slides=int(os.environ.get("PF_TIME_SLIDES", "4")), width=40000, height=30000, dtype="bf16", gpus=1)
 pf, plan, slides = bench.build_slides(args, 0, 1)
 scfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=[(0.25, 1.0)], seed=plan.sampler_seed)
 L = MultiCropLoader(slides, scfg, MultiCropConfig(), batch_size=1024)
