@@ -35,3 +35,17 @@ def test_bench_default_line(cuda):
     assert e["value"] > 0 and e["unit"] == d["unit"] and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 3 * 4  # sampler + params + two multi-crop groups per step
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+def test_bench_reference_arm_line(cuda):
+    """--impl reference (the reference pipeline on the host cores): its own line with impl,
+    cpu_baseline and a zero-transfer e2e.  Runs with the GPU tests (slow on a small host)."""
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1", "--warmup", "1"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 1 and d["warmup"] == 1
+    assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["kind"] in ("port", "reference")
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
