@@ -463,11 +463,15 @@ def run_b200(args):
     st = feed.sampler.check()
     e2e = None
     if not args.no_e2e:
-        e2e = feed.e2e_fn(pf, feed.loader, max(3, min(args.steps, 10)), torch)
+        e2e_steps = max(3, min(args.steps, 10))
         if world > 1:
-            te = torch.tensor([e2e["value"]], dtype=torch.float64, device="cuda")
-            dist.all_reduce(te, op=dist.ReduceOp.SUM)
-            e2e["value"] = float(te.item())
+            dist.barrier()
+        e2e = feed.e2e_fn(pf, feed.loader, e2e_steps, torch)
+        if world > 1:  # whole job: every rank's patches over the slowest rank's wall time
+            n_rank = e2e_steps * feed.loader.batch_size
+            te = torch.tensor([n_rank / e2e["value"]], dtype=torch.float64, device="cuda")
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            e2e["value"] = round(world * n_rank / float(te.item()), 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, steps=args.cpu_steps)
