@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
+    # test hooks (tests/test_gpu_multirank.py): N ranks on one GPU over gloo, per-rank stream dump
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--device", type=int, default=None, help="CUDA device of every rank (default LOCAL_RANK)")
+    ap.add_argument("--dump-dir", default=None, help="each rank writes its first batch's specs + crop params")
     args = ap.parse_args()
     if args.mixed_mpp:
         args.config = "3"
@@ -225,7 +229,8 @@ def make_feed(args, pf, plan, slides, rank, src_size=224, n_local=8, patch=224):
         mpps = [(0.25 * patch / 224.0, 1.0)]
     scfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=mpps, seed=plan.sampler_seed)
     mc = MultiCropConfig(n_local=n_local)
-    loader = MultiCropLoader(slides, scfg, mc, batch_size=args.batch, rank=rank, dtype=args.dtype, rounds=rounds)
+    loader = MultiCropLoader(slides, scfg, mc, batch_size=args.batch, rank=rank, dtype=args.dtype, rounds=rounds,
+                             aug_seed=plan.philox_seed)
     tag = {"2": "C2", "3": "C3 (mpp U{0.25,0.5,1,2})", "4": "C4", "5": f"C5 point (patch {patch}->224, L={n_local})"}[args.config]
     if args.config == "4":
         r = getattr(args, "residency", None) or {}
@@ -334,7 +339,7 @@ def _time_e2e(step, steps, n, torch, h2d, d2h, path):
 def timed_run(feed, args, torch, dist, world, local, N):
     """W warm-up steps, then K timed steps between barriers; per-stage CUDA events."""
     loader = feed.loader
-    clk = ClockSampler(local).__enter__()  # sampling spans warm-up + timed steps (all under load)
+    clk = ClockSampler(torch.cuda.current_device()).__enter__()  # sampling spans warm-up + timed steps (all under load)
     for _ in range(max(args.warmup, 0)):
         loader.next_batch()
     torch.cuda.synchronize()
@@ -358,7 +363,7 @@ def timed_run(feed, args, torch, dist, world, local, N):
     clk.__exit__(None, None, None)
     launches = N.launches() - l0
     elapsed_ms = start.elapsed_time(end)
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda" if args.dist_backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
@@ -451,14 +456,26 @@ def run_b200(args):
     from paper_2404_15217_b200 import _native as N
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    dev = local if args.device is None else args.device
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     pf, plan, slides = build_slides(args, rank, world)
     if args.config == "5":
         run_sweep(args, pf, plan, slides, rank, world, local, torch, dist, N)
         return
     feed = make_feed(args, pf, plan, slides, rank)
+    if args.dump_dir:  # the rank's first batch (step 0): specs + crop parameters
+        out = feed.loader.next_batch()
+        torch.cuda.synchronize()
+        Path(args.dump_dir).mkdir(parents=True, exist_ok=True)
+        extra = {"params": out["params"].cpu().numpy()} if "params" in out else {}
+        np.savez(Path(args.dump_dir) / f"rank{rank}.npz", specs=out["specs"].cpu().numpy(), rank=rank, world=world,
+                 sampler_seed=plan.sampler_seed, philox_seed=plan.philox_seed,
+                 slide_indices=np.array(plan.slide_indices), **extra)
     elapsed_ms, stage_ms, launches, clocks = timed_run(feed, args, torch, dist, world, local, N)
     st = feed.sampler.check()
     e2e = None
@@ -469,7 +486,8 @@ def run_b200(args):
         e2e = feed.e2e_fn(pf, feed.loader, e2e_steps, torch)
         if world > 1:  # whole job: every rank's patches over the slowest rank's wall time
             n_rank = e2e_steps * feed.loader.batch_size
-            te = torch.tensor([n_rank / e2e["value"]], dtype=torch.float64, device="cuda")
+            te = torch.tensor([n_rank / e2e["value"]], dtype=torch.float64,
+                              device="cuda" if args.dist_backend == "nccl" else "cpu")
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
             e2e["value"] = round(world * n_rank / float(te.item()), 1)
     cpu = None

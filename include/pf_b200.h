@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 1
+#define PF_ABI_VERSION 2
 #define PF_MAX_LEVELS 12
 #define PF_MAX_MPPS 8
 #define PF_MAX_CROPS 16
@@ -86,6 +86,10 @@ typedef struct pf_slide_desc {
     int32_t n_levels;
     int32_t tile_size;
     double base_mpp;
+    /* 0, or the device address of an int32 fault word: a read that resolves
+     * to the zero hole (slot 0) of a compacted level stores
+     * PF_ERR_OUT_OF_BOUNDS there (pf_slide_status reads and clears it). */
+    uint64_t status_word;
 } pf_slide_desc;
 
 /* One patch to extract: the reference's PatchSpec (pkg/sampler.py:61-103)
@@ -102,6 +106,38 @@ typedef struct pf_patch_spec {
     int32_t sx, sy;    /* rha(x/ds_L), rha(y/ds_L) — filled on device */
     int32_t flags;
 } pf_patch_spec;
+
+/* ------------------------------------------------------------------------ */
+/* Library-owned slide handles (ownership row of SURVEY §8(b)): the pyramid   */
+/* lives in HBM allocated by the library; callers without torch create a      */
+/* slide, upload level-0 pixels (then the pyramid is box-filtered on device)  */
+/* or store tiles, and pass pf_slide_get_desc's descriptor (copied into a     */
+/* device array) to the batched entry points.  Replaces open_slide /          */
+/* SlideRecord + TileCache-backed reads (pkg/store.py:123-237, 270-319,       */
+/* 727-751) for a resident pyramid.                                          */
+/* ------------------------------------------------------------------------ */
+typedef struct pf_slide pf_slide;
+/* Level dims as ingest_image (pkg/store.py:496-498): ceil-divide by the
+ * factor until max(dim) <= tile_size; mpp_l = base_mpp * factor^l. */
+int pf_slide_create(int32_t width, int32_t height, double base_mpp, int32_t tile_size,
+                    int32_t downsample_factor, pf_slide** out);
+int pf_slide_destroy(pf_slide* slide); /* synchronises the device */
+int pf_slide_get_desc(const pf_slide* slide, pf_slide_desc* out_host);
+/* Level-0 RGB rows (row_stride bytes apart, 0 = 3 * width), host or device
+ * memory, tiled into level 0; levels 1.. then built with pf_build_level.
+ * Host uploads synchronise the stream per 256-row chunk. */
+int pf_slide_upload_level0(pf_slide* slide, const uint8_t* hwc, int64_t row_stride, int32_t on_host,
+                           void* stream);
+/* One decoded store tile (tile_dims-cropped, pkg/store.py:140-149) from host
+ * memory into its slot; then pf_slide_build_pyramid if upper levels are not
+ * uploaded too. */
+int pf_slide_upload_tile(pf_slide* slide, int32_t level, int32_t tx, int32_t ty, const uint8_t* tile_hwc_host,
+                         int32_t tw, int32_t th, void* stream);
+int pf_slide_build_pyramid(pf_slide* slide, void* stream);
+/* Synchronise `stream` and read the descriptor's fault word: PF_ERR_OUT_OF_BOUNDS
+ * (store.OutOfBoundsError, pkg/store.py:66) if a read since the last clear hit
+ * the zero hole of a compacted level, else PF_OK.  clear != 0 resets it. */
+int pf_slide_status(const pf_slide_desc* desc_host, int32_t clear, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Library                                                                   */
@@ -145,6 +181,23 @@ int pf_plan_regions(const pf_slide_desc* slides_dev, pf_patch_spec* specs_dev, i
 int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_spec* specs_dev, int32_t n,
                     int32_t out_size, int32_t dtype, int32_t layout, const float* mean3,
                     const float* std3, void* out, void* stream);
+
+/* Whether pf_read_regions' fused kernel takes a window of `side` px resampled
+ * to out_size (its shared-memory plan holds a band of >= 4 source rows and
+ * <= 32 taps: down-ratios up to ~15 at out_size <= 512).  Other requests go
+ * through pf_read_region_generic. */
+int pf_read_region_fits(int32_t side, int32_t out_size, int32_t dtype, int32_t* fits);
+
+/* Slide.read_region (pkg/store.py:651-688) for ONE spec of any size: PIL's
+ * two BILINEAR passes (22-bit taps, bit-exact) through a global uint8
+ * intermediate in `scratch_dev` (pf_read_region_generic_scratch_bytes), or
+ * the clamped window itself when side == out_size.  `spec` is a HOST record
+ * with level/side/sx/sy filled; `slides_dev` the device descriptor array.
+ * Output as pf_read_regions for one patch ([S, S, 3] or [3, S, S]). */
+int pf_read_region_generic_scratch_bytes(int32_t side, int32_t out_size, int64_t* bytes);
+int pf_read_region_generic(const pf_slide_desc* slides_dev, const pf_patch_spec* spec, int32_t out_size,
+                           int32_t dtype, int32_t layout, const float* mean3, const float* std3,
+                           void* scratch_dev, int64_t scratch_bytes, void* out, void* stream);
 
 /* normalize_patch (pkg/pipeline.py:152-155) on an HWC uint8 device buffer of
  * n_pixels RGB pixels: out = (v/255 - mean[c]) / std[c] in FP32 (same layout),

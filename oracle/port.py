@@ -239,6 +239,8 @@ def points_in_polygon(points: np.ndarray, rings) -> np.ndarray:  # foreground.py
 
 
 def polygon_from_mask(bits: np.ndarray, scale: float, min_region_px: float = 64.0):  # foreground.py:169-220
+    if not np.asarray(bits).any():  # foreground.py:178-179 (EmptyForegroundError is a ValueError)
+        raise ValueError("mask contains no foreground pixels")
     padded = np.pad(np.asarray(bits).astype(np.float64), 1)
     rings = []
     for ct in find_contours_binary(padded):
@@ -255,6 +257,8 @@ def polygon_from_mask(bits: np.ndarray, scale: float, min_region_px: float = 64.
         if (shoelace(ring) > 0) != (depth % 2 == 0):
             ring = ring[::-1]
         out.append(ring / scale)
+    if not out:  # foreground.py:196-199
+        raise ValueError(f"no region of at least {min_region_px} px^2 in the mask")
     return out
 
 

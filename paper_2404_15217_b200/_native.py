@@ -54,6 +54,7 @@ class SlideDesc(C.Structure):
         ("n_levels", C.c_int32),
         ("tile_size", C.c_int32),
         ("base_mpp", C.c_double),
+        ("status_word", C.c_uint64),
     ]
 
 
@@ -159,7 +160,7 @@ CROP_DTYPE = np.dtype(
 assert CROP_DTYPE.itemsize == 64
 
 assert C.sizeof(SamplerState) == 80
-assert C.sizeof(SlideDesc) == 96 + 96 + 96 + 5 * 48 + 8 + 8
+assert C.sizeof(SlideDesc) == 96 + 96 + 96 + 5 * 48 + 8 + 8 + 8
 
 
 class _Lib:
@@ -182,6 +183,16 @@ class _Lib:
             "pf_thumbnail": ([C.POINTER(SlideDesc), i32, i32, vp, vp], C.c_int),
             "pf_plan_regions": ([vp, vp, i32, vp], C.c_int),
             "pf_read_regions": ([vp, vp, i32, i32, i32, i32, vp, vp, vp, vp], C.c_int),
+            "pf_read_region_fits": ([i32, i32, i32, C.POINTER(i32)], C.c_int),
+            "pf_slide_create": ([i32, i32, dbl, i32, i32, C.POINTER(vp)], C.c_int),
+            "pf_slide_destroy": ([vp], C.c_int),
+            "pf_slide_get_desc": ([vp, C.POINTER(SlideDesc)], C.c_int),
+            "pf_slide_upload_level0": ([vp, vp, i64, i32, vp], C.c_int),
+            "pf_slide_upload_tile": ([vp, i32, i32, i32, vp, i32, i32, vp], C.c_int),
+            "pf_slide_build_pyramid": ([vp, vp], C.c_int),
+            "pf_slide_status": ([C.POINTER(SlideDesc), i32, vp], C.c_int),
+            "pf_read_region_generic_scratch_bytes": ([i32, i32, C.POINTER(i64)], C.c_int),
+            "pf_read_region_generic": ([vp, vp, i32, i32, i32, vp, vp, vp, i64, vp, vp], C.c_int),
             "pf_normalize": ([vp, i64, i32, vp, vp, vp, vp], C.c_int),
             "pf_mask": ([vp, i32, i32, i32, dbl, i32, vp, vp, vp], C.c_int),
             "pf_polygon_trace": (
@@ -217,7 +228,7 @@ class _Lib:
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res
-        if L.pf_abi_version() != 1:
+        if L.pf_abi_version() != 2:
             raise errors.NativeLibraryError("libpfb200 ABI version mismatch")
 
     @classmethod

@@ -41,7 +41,11 @@ __device__ __forceinline__ const uint8_t* tile_ptr(const pf_slide_desc& s, int l
     const uint8_t* base = reinterpret_cast<const uint8_t*>(s.level_ptr[level]);
     const size_t t = (size_t)ty * s.tiles_x[level] + tx;
     const int32_t* map = reinterpret_cast<const int32_t*>(s.tile_map[level]);
-    return base + (map ? (size_t)__ldg(map + t) : t) * tile_bytes;
+    if (!map) return base + t * tile_bytes;
+    const int32_t slot = __ldg(map + t);
+    if (slot == 0 && s.status_word)  // the zero hole: the read plan missed this tile (fail loudly)
+        *reinterpret_cast<volatile int32_t*>(s.status_word) = PF_ERR_OUT_OF_BOUNDS;
+    return base + (size_t)slot * tile_bytes;
 }
 
 // Address of pixel (X, Y) in a padded tile-major level (see pf_b200.h).

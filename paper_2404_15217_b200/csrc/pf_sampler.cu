@@ -266,11 +266,12 @@ constexpr int kDrawCache = 256;
 
 __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
     pf_sampler_config cfg, const pf_sampler_slide* slides, const pf_slide_desc* descs, pf_sampler_state* state,
-    SamplerWs ws, int window, int n, int use_table, int finish, int bitmaps_in_smem, int2* emit_list,
+    SamplerWs ws, int window, int n, int use_table, int finish, int bitmaps_in_smem, int next_table, int2* emit_list,
     pf_patch_spec* out) {
     extern __shared__ __align__(16) uint32_t s_dyn[];
     __shared__ int16_t s_draw[kDrawCache];
     __shared__ int s_first, s_last;
+    __shared__ int64_t s_seq0;  // stream seq at entry: warp 0 rewrites *state at exit
     WalkState w;
     load_ws(state, w);
     if (w.status != PF_OK || w.emitted >= n) return;
@@ -281,6 +282,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
     if (tid == 0) {
         s_first = w.emitted;
         s_last = w.emitted;
+        s_seq0 = state->seq;
     }
     if (use_table) {
         const uint32_t* bm_all = ws.bitmaps;
@@ -289,6 +291,47 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
             bm_all = s_dyn;
         }
         __syncthreads();
+        // next_table: next accepted offset of every (slide, window offset) -- a parallel suffix
+        // search over the accept bitmaps -- so each slide draw of the walk is one shared load.
+        // Layout after the bitmaps: nextw[n_slides][words] (first non-zero word at or after w),
+        // na[n_slides][window] (uint16; 0xffff = none).
+        uint16_t* nextw = reinterpret_cast<uint16_t*>(s_dyn + cfg.n_slides * words);
+        uint16_t* na = nextw + ((cfg.n_slides * words + 1) & ~1);
+        if (next_table) {
+            const int warp = tid >> 5, nwarps = kWalkThreads / 32;
+            for (int sl = warp; sl < cfg.n_slides; sl += nwarps) {  // one warp per slide, chunks from the end
+                const uint32_t* bm = bm_all + (size_t)sl * words;
+                int carry = words;
+                for (int base = ((words - 1) >> 5) << 5; base >= 0; base -= 32) {
+                    const int wi = base + lane;
+                    int v = (wi < words && bm[wi] != 0u) ? wi : words;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int u = __shfl_down_sync(0xffffffffu, v, o);
+                        if (lane + o < 32) v = min(v, u);
+                    }
+                    v = min(v, carry);
+                    if (wi < words) nextw[sl * words + wi] = (uint16_t)v;
+                    carry = __shfl_sync(0xffffffffu, v, 0);
+                }
+            }
+            __syncthreads();
+            for (int i = tid; i < cfg.n_slides * window; i += kWalkThreads) {
+                const int sl = i / window, a = i - sl * window;
+                const uint32_t* bm = bm_all + (size_t)sl * words;
+                const int wd = a >> 5;
+                const uint32_t m = bm[wd] & (0xffffffffu << (a & 31));
+                int f = 0xffff;
+                if (m) {
+                    f = wd * 32 + __ffs(m) - 1;
+                } else if (wd + 1 < words) {
+                    const int w2 = nextw[sl * words + wd + 1];
+                    if (w2 < words) f = w2 * 32 + __ffs(bm[w2]) - 1;
+                }
+                na[i] = (uint16_t)f;
+            }
+            __syncthreads();
+        }
         if (tid < 32) {
             const uint64_t m0 = w.c_mpp;
             const int wlim = min(window, *ws.reject_at);
@@ -298,6 +341,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                 if (w.cur_slide < 0) {
                     if (draw_pos == draw_cnt) {  // refill: 32 lanes draw the next kDrawCache counters
                         draw_base = w.c_slide;
+                        __syncwarp();  // every lane has read its last s_draw entry
                         for (int i = lane; i < kDrawCache; i += 32) {
                             const uint64_t v = stream_u64(cfg.key_slide, draw_base + 1 + (uint64_t)i);
                             int sidx;
@@ -333,7 +377,10 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                 const int budget = max_att - w.cur_used;
                 const int span = min(budget, wlim - a0);
                 int found = -1;
-                if (span > 0) {
+                if (span > 0 && next_table) {
+                    const int f = na[w.cur_slide * window + a0];
+                    if (f < a0 + span) found = f;
+                } else if (span > 0) {
                     const uint32_t* bm = bm_all + (size_t)w.cur_slide * words;
                     const int wfirst = a0 >> 5, wlast = (a0 + span - 1) >> 5;
                     // common case first (acceptance ~0.5): the next accepted offset lies in a0's word
@@ -392,7 +439,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
         __syncthreads();
         // materialise the emitted specs in parallel
         const int first = s_first, last = s_last;
-        const int64_t seq0 = state->seq;
+        const int64_t seq0 = s_seq0;
         for (int i = first + tid; i < last; i += kWalkThreads) {
             const int2 e = emit_list[i - first];
             const int4 cd = ws.cands[(size_t)e.x * window + e.y];
@@ -511,7 +558,12 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     const size_t eval_smem = (size_t)warps * overlap_smem_bytes_chunked(cfg->grid);
     const size_t bm_bytes_all = (size_t)cfg->n_slides * (window / 32) * 4;
     const int bm_in_smem = rounds > 0 && bm_bytes_all <= 160 * 1024;
-    const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid), bm_in_smem ? bm_bytes_all : (size_t)0);
+    // next-accepted-offset table beside the bitmaps (uint16 offsets: window < 0xffff)
+    const size_t nt_bytes = bm_bytes_all + ((size_t)cfg->n_slides * (window / 32) + 1) / 2 * 4 +
+                            (size_t)cfg->n_slides * window * 2;
+    const int next_table = bm_in_smem && window < 0xffff && nt_bytes <= 200 * 1024;
+    const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid),
+                                      next_table ? nt_bytes : (bm_in_smem ? bm_bytes_all : (size_t)0));
     rc = check_cuda(cudaFuncSetAttribute(sample_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)walk_smem),
                     "cudaFuncSetAttribute");
     if (rc) return rc;
@@ -536,12 +588,12 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
         if ((rc = after_launch("sample_eval_kernel"))) return rc;
         sample_walk_kernel<<<1, kWalkThreads, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws,
                                                                 window, n, 1, r == rounds - 1, bm_in_smem,
-                                                                ws.emits, out_dev);
+                                                                next_table, ws.emits, out_dev);
         if ((rc = after_launch("sample_walk_kernel"))) return rc;
     }
     if (rounds == 0) {
         sample_walk_kernel<<<1, kWalkThreads, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws,
-                                                                window, n, 0, 1, 0, nullptr, out_dev);
+                                                                window, n, 0, 1, 0, 0, nullptr, out_dev);
         if ((rc = after_launch("sample_walk_kernel"))) return rc;
     }
     return PF_OK;

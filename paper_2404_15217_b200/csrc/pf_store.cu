@@ -438,6 +438,98 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
     }
 }
 
+// ---------------------------------------------------------------------------
+// General read_region for one spec whose window does not fit the fused kernel's shared-memory
+// plan (down-ratio above ~15, or out_size > 512): PIL's two passes (Resample.c,
+// ImagingResampleHorizontal / Vertical, 22-bit taps) through a global uint8 intermediate.
+// Rare requests (the reference's PIL path accepts any ratio); not on the training hot path.
+// ---------------------------------------------------------------------------
+// coefficient table of one axis (side -> S): xmin[S], xsize[S], w[S * K] (int32, zero padded);
+// the double weights are staged in w as doubles first (K doubles per output, 2K int32 slots)
+__global__ void generic_coeffs_kernel(int side, int S, int K, int* xmin_t, int* xsize_t, int32_t* w_t, double* wd) {
+    const AxisPlan p = axis_plan(side, S);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+        const double center = p.scale * ((double)i + 0.5);
+        int xmin = (int)(center - p.support + 0.5);
+        if (xmin < 0) xmin = 0;
+        int xmax = (int)(center + p.support + 0.5);
+        if (xmax > side) xmax = side;
+        int xs = xmax - xmin;
+        if (xs < 0) xs = 0;
+        if (xs > K) xs = K;
+        double* w = wd + (size_t)i * K;
+        double ww = 0.0;
+        for (int x = 0; x < xs; ++x) {
+            const double v = triangle(((double)(x + xmin) - center + 0.5) * p.invscale);
+            w[x] = v;
+            ww += v;
+        }
+        if (ww != 0.0)
+            for (int x = 0; x < xs; ++x) w[x] = w[x] / ww;
+        xmin_t[i] = xmin;
+        xsize_t[i] = xs;
+        for (int k = 0; k < K; ++k) w_t[(size_t)i * K + k] = k < xs ? quantise_weight(w[k], 22) : 0;
+    }
+}
+
+// horizontal pass: window rows [0, side) -> inter[side][S][3] (rows clamped: _read_window's
+// +-1 px edge replication; columns clamped likewise)
+__global__ void generic_hpass_kernel(const pf_slide_desc* slides, pf_patch_spec sp, int S, int K, const int* xmin_t,
+                                     const int* xsize_t, const int32_t* w_t, uint8_t* inter) {
+    const pf_slide_desc& sd = slides[sp.slide];
+    const int L = sp.level, LW = sd.width[L], LH = sd.height[L];
+    const int r = blockIdx.y;
+    const int Y = clampi(sp.sy + r, 0, LH - 1);
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < S; x += gridDim.x * blockDim.x) {
+        const int xm = xmin_t[x], xs = xsize_t[x];
+        const int32_t* w = w_t + (size_t)x * K;
+        int32_t a0 = 1 << 21, a1 = 1 << 21, a2 = 1 << 21;
+        for (int k = 0; k < xs; ++k) {
+            const uint8_t* p = level_pixel(sd, L, clampi(sp.sx + xm + k, 0, LW - 1), Y);
+            a0 += (int32_t)p[0] * w[k];
+            a1 += (int32_t)p[1] * w[k];
+            a2 += (int32_t)p[2] * w[k];
+        }
+        uint8_t* d = inter + ((size_t)r * S + x) * 3;
+        d[0] = clip_shift(a0, 22);
+        d[1] = clip_shift(a1, 22);
+        d[2] = clip_shift(a2, 22);
+    }
+}
+
+// vertical pass (or the passthrough copy when the window already is S x S) -> normalised output
+template <int kDtype>
+__global__ void generic_vpass_kernel(const pf_slide_desc* slides, pf_patch_spec sp, int S, int K, const int* xmin_t,
+                                     const int* xsize_t, const int32_t* w_t, const uint8_t* inter, int layout,
+                                     NormParams np, void* out) {
+    const int y = blockIdx.y;
+    const size_t plane = (size_t)S * S;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < S; x += gridDim.x * blockDim.x) {
+        uint8_t px[3];
+        if (inter) {
+            const int ym = xmin_t[y], ys = xsize_t[y];
+            const int32_t* w = w_t + (size_t)y * K;
+            int32_t a[3] = {1 << 21, 1 << 21, 1 << 21};
+            for (int k = 0; k < ys; ++k) {
+                const uint8_t* p = inter + ((size_t)(ym + k) * S + x) * 3;
+                a[0] += (int32_t)p[0] * w[k];
+                a[1] += (int32_t)p[1] * w[k];
+                a[2] += (int32_t)p[2] * w[k];
+            }
+            for (int c = 0; c < 3; ++c) px[c] = clip_shift(a[c], 22);
+        } else {  // side == S: the window itself (clamped at the level edge)
+            const pf_slide_desc& sd = slides[sp.slide];
+            const int L = sp.level;
+            const uint8_t* p = level_pixel(sd, L, clampi(sp.sx + x, 0, sd.width[L] - 1), clampi(sp.sy + y, 0, sd.height[L] - 1));
+            px[0] = p[0], px[1] = p[1], px[2] = p[2];
+        }
+        for (int c = 0; c < 3; ++c) {
+            const size_t idx = layout == PF_HWC ? ((size_t)y * S + x) * 3 + c : c * plane + (size_t)y * S + x;
+            store_px<kDtype>(out, idx, px[c], c, np);
+        }
+    }
+}
+
 template <int kDtype>
 __global__ void normalize_kernel(const uint8_t* in, int64_t n, NormParams np, void* out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -550,3 +642,91 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
     return after_launch("read_regions_kernel");
 }
 
+
+namespace {
+// The fused kernel's shared-memory plan for a resampled window (read_regions_kernel above):
+// whether a band of >= 4 staged source rows fits.
+bool fused_fits(int side, int S, int dtype) {
+    if (S > 512) return false;
+    if (side == S) return true;
+    const AxisPlan ap = axis_plan(side, S);
+    const int K = ap.ksize;
+    if (K > 32) return false;
+    const int osz = dtype == PF_F32 ? 4 : (dtype == PF_BF16 ? 2 : 1);
+    const int lut = (3 * 256 * osz + 15) & ~15;
+    const int work_bytes = kRRSmem - lut;
+    const int tab = (((2 * S + S * K) * 4) + 15) & ~15;
+    const int buf_bytes = work_bytes - (tab + 16);
+    const int nch = (15 + side * 3 + 15) / 16;  // worst-case offset 15
+    const int pitch = nch * 16 + 16;
+    const int cap = (buf_bytes - 3 * S * 4) / (2 * pitch + 3 * S);
+    return cap >= 4;
+}
+}  // namespace
+
+extern "C" int pf_read_region_fits(int32_t side, int32_t out_size, int32_t dtype, int32_t* fits) {
+    if (side < 1 || out_size < 1 || !fits) return fail(PF_ERR_INVALID_ARG, "pf_read_region_fits: bad arguments");
+    *fits = fused_fits(side, out_size, dtype) ? 1 : 0;
+    return PF_OK;
+}
+
+extern "C" int pf_read_region_generic_scratch_bytes(int32_t side, int32_t out_size, int64_t* bytes) {
+    if (side < 1 || out_size < 1 || !bytes) return fail(PF_ERR_INVALID_ARG, "pf_read_region_generic_scratch_bytes: bad arguments");
+    const int64_t K = axis_plan(side, out_size).ksize;
+    const int64_t S = out_size;
+    *bytes = 2 * S * 4 + S * K * 4 + S * K * 8 + (int64_t)side * S * 3 + 64;
+    return PF_OK;
+}
+
+extern "C" int pf_read_region_generic(const pf_slide_desc* slides_dev, const pf_patch_spec* spec, int32_t out_size,
+                                      int32_t dtype, int32_t layout, const float* mean3, const float* std3,
+                                      void* scratch_dev, int64_t scratch_bytes, void* out, void* stream) {
+    if (!slides_dev || !spec || out_size < 1 || !out || spec->side < 1)
+        return fail(PF_ERR_INVALID_ARG, "pf_read_region_generic: bad arguments");
+    if (layout != PF_HWC && layout != PF_NCHW) return fail(PF_ERR_INVALID_ARG, "pf_read_region_generic: bad layout");
+    if (dtype != PF_U8 && dtype != PF_F32 && dtype != PF_BF16)
+        return fail(PF_ERR_INVALID_ARG, "pf_read_region_generic: bad dtype");
+    const int S = out_size, side = spec->side;
+    NormParams np;
+    for (int c = 0; c < 3; ++c) {
+        np.mean[c] = mean3 ? mean3[c] : 0.5f;
+        np.stdv[c] = std3 ? std3[c] : 0.5f;
+    }
+    cudaStream_t st = as_stream(stream);
+    const int K = axis_plan(side, S).ksize;
+    int* xmin_t = nullptr;
+    int* xsize_t = nullptr;
+    int32_t* w_t = nullptr;
+    uint8_t* inter = nullptr;
+    if (side != S) {
+        int64_t need = 0;
+        pf_read_region_generic_scratch_bytes(side, S, &need);
+        if (!scratch_dev || scratch_bytes < need)
+            return fail(PF_ERR_CAPACITY, "pf_read_region_generic: scratch too small");
+        uint8_t* base = static_cast<uint8_t*>(scratch_dev);
+        double* wd = reinterpret_cast<double*>(base);
+        xmin_t = reinterpret_cast<int*>(base + (size_t)S * K * 8);
+        xsize_t = xmin_t + S;
+        w_t = xsize_t + S;
+        inter = reinterpret_cast<uint8_t*>(w_t + (size_t)S * K);
+        generic_coeffs_kernel<<<(S + 127) / 128, 128, 0, st>>>(side, S, K, xmin_t, xsize_t, w_t, wd);
+        int rc = after_launch("generic_coeffs_kernel");
+        if (rc) return rc;
+        generic_hpass_kernel<<<dim3((S + 127) / 128, side), 128, 0, st>>>(slides_dev, *spec, S, K, xmin_t, xsize_t,
+                                                                         w_t, inter);
+        if ((rc = after_launch("generic_hpass_kernel"))) return rc;
+    }
+    const dim3 grid((S + 127) / 128, S);
+    switch (dtype) {
+        case PF_U8:
+            generic_vpass_kernel<PF_U8><<<grid, 128, 0, st>>>(slides_dev, *spec, S, K, xmin_t, xsize_t, w_t, inter, layout, np, out);
+            break;
+        case PF_F32:
+            generic_vpass_kernel<PF_F32><<<grid, 128, 0, st>>>(slides_dev, *spec, S, K, xmin_t, xsize_t, w_t, inter, layout, np, out);
+            break;
+        default:
+            generic_vpass_kernel<PF_BF16><<<grid, 128, 0, st>>>(slides_dev, *spec, S, K, xmin_t, xsize_t, w_t, inter, layout, np, out);
+            break;
+    }
+    return after_launch("generic_vpass_kernel");
+}

@@ -97,10 +97,10 @@ _RRC_TABLES: dict = {}
 def rrc_table(src_size: int, out_size: int) -> int:
     """Device address of the RandomResizedCrop tap table for (src_size -> out_size), built once
     per process (pf_rrc_table_build) and kept alive here."""
-    key = (src_size, out_size)
+    torch = N.require_cuda()
+    key = (torch.cuda.current_device(), src_size, out_size)  # the table lives on the current device
     t = _RRC_TABLES.get(key)
     if t is None:
-        torch = N.require_cuda()
         nbytes = C.c_int64(0)
         N.check(N.lib().pf_rrc_table_bytes(src_size, out_size, C.byref(nbytes)), "pf_rrc_table_bytes")
         t = torch.empty((nbytes.value,), dtype=torch.uint8, device="cuda")
@@ -162,7 +162,7 @@ class MultiCropLoader:
 
     def __init__(self, slides, sampler_config, mc_config: MultiCropConfig | None = None, *, batch_size: int = 1024,
                  rank: int = 0, dtype: str = "bf16", mean=IMAGENET_MEAN, std=IMAGENET_STD, window=None, rounds: int = 2,
-                 prefetch: bool = True, cap: int | None = None):
+                 prefetch: bool = True, cap: int | None = None, aug_seed: int | None = None):
         torch = N.require_cuda()
         from .sampler import CappedSampler, GpuSampler
         from .store import SlideSet
@@ -176,7 +176,9 @@ class MultiCropLoader:
         self.specs_from = self.sampler if cap is None else CappedSampler(self.sampler, cap, sampler_config.seed)
         self.batch_size = batch_size
         self.rank = rank
-        self.seed = sampler_config.seed
+        # Philox(seed, rank, step) for the crop parameters: the run's base seed (default: the
+        # sampler's, which under sharding is already seed + rank)
+        self.seed = sampler_config.seed if aug_seed is None else int(aug_seed)
         self.dtype = dtype
         self.mean, self.std = mean, std
         self.step = 0
@@ -260,6 +262,15 @@ class MultiCropLoader:
         self.step += 1
         return {"global_crops": self.out_global, "local_crops": self.out_local, "specs": specs,
                 "params": self.params}
+
+    def check(self) -> None:
+        """Synchronise and raise on a failed stream: NoSamplableSlideError from the sampler state,
+        OutOfBoundsError if a crop read a tile outside a compacted slide's resident set."""
+        torch = N.require_cuda()
+        self.drain()
+        torch.cuda.current_stream().synchronize()
+        self.sampler.check()
+        self.slide_set.check_status()
 
     def drain(self) -> None:
         """Wait for the prefetched sampler work (so the sampler state is final)."""

@@ -66,9 +66,14 @@ class LoaderRun:
 def run_loader(specs, slides, config: LoaderConfig | None = None, batch: int | None = None) -> LoaderRun:
     """Load every spec exactly once (pkg/pipeline.py:79-149) with batched GPU reads.
 
-    ``slides``: a GpuSlide or mapping slide_id -> GpuSlide.  Output order is the
-    input order (``ordered`` is honoured trivially); per-spec failures follow
-    ``on_error``.
+    ``slides``: a GpuSlide or mapping slide_id -> GpuSlide.  Specs are pulled from the
+    iterable in chunks of ``batch`` (default max(prefetch_depth, 64)); a chunk is planned on the
+    host, read in one device call per out_size, and emitted in input order.  Failures are
+    handled at the failing spec's position, as the reference's ordered consumer does
+    (pipeline.py:97-124): under "raise" every earlier spec is yielded before LoaderError, under
+    "skip" the failure joins ``LoaderRun.errors`` when iteration reaches it.  ``ordered=False``
+    may emit in any order (reference: completion order); this loader's completion order is the
+    input order.  ``concurrency`` has no device meaning and is only validated.
     """
     config = config or LoaderConfig()
     if isinstance(slides, GpuSlide):
@@ -82,40 +87,45 @@ def run_loader(specs, slides, config: LoaderConfig | None = None, batch: int | N
             raise LoaderError(f"patch seq {spec.seq} failed: {exc}") from exc
         errors.append(LoaderFailure(spec, exc))
 
-    def flush(chunk):
-        good, reqs = [], []
-        for sp in chunk:
+    def load_chunk(chunk):
+        """[(pixels or None, exception or None)] in chunk order."""
+        res: list = [(None, None)] * len(chunk)
+        good: dict = {}  # out_size -> [(position, request)]
+        for i, sp in enumerate(chunk):
             si = sset.index.get(sp.slide_id)
             if si is None:
-                fail(sp, LoaderError(f"no open slide for id {sp.slide_id!r}"))
+                res[i] = (None, LoaderError(f"no open slide for id {sp.slide_id!r}"))
                 continue
+            req = (si, sp.rect(), sp.target_mpp, sp.out_size)
             try:
-                plan_specs([(si, sp.rect(), sp.target_mpp, sp.out_size)], sset.records)
-            except Exception as exc:  # noqa: BLE001 - policy decides
-                fail(sp, exc)
+                row = plan_specs([req], sset.records)[0]  # the reference's read_region checks, per spec
+                sset.slides[si].require_resident(row)
+            except Exception as exc:  # noqa: BLE001 - the error policy decides
+                res[i] = (None, exc)
                 continue
-            good.append(sp)
-            reqs.append((si, sp.rect(), sp.target_mpp, sp.out_size))
-        # group by out_size (one device call each), then restore input order
-        out = {}
-        for size in sorted({sp.out_size for sp in good}):
-            idx = [i for i, sp in enumerate(good) if sp.out_size == size]
-            arr = plan_specs([reqs[i] for i in idx], sset.records)
+            good.setdefault(sp.out_size, []).append((i, req))
+        for size, items in good.items():
+            arr = plan_specs([r for _, r in items], sset.records)
             pix = sset.read_regions(arr, size).cpu().numpy()
-            for j, i in enumerate(idx):
-                out[i] = pix[j]
-        for i, sp in enumerate(good):
-            yield sp, out[i]
+            for j, (i, _) in enumerate(items):
+                res[i] = (pix[j], None)
+        return res
 
     def gen():
-        chunk = []
-        for sp in specs:
-            chunk.append(sp)
-            if len(chunk) >= bsz:
-                yield from flush(chunk)
-                chunk = []
-        if chunk:
-            yield from flush(chunk)
+        it = iter(specs)
+        while True:
+            chunk = []
+            for sp in it:
+                chunk.append(sp)
+                if len(chunk) >= bsz:
+                    break
+            if not chunk:
+                return
+            for sp, (pix, exc) in zip(chunk, load_chunk(chunk)):
+                if exc is not None:
+                    fail(sp, exc)
+                    continue
+                yield sp, pix
 
     return LoaderRun(gen(), errors)
 

@@ -278,6 +278,7 @@ class GpuSampler:
         st.cur_slide = -1
         self.state.copy_(torch.frombuffer(bytearray(bytes(st)), dtype=torch.uint8))
         self._ws = None
+        self._ws_stream = None
         self._ws_window = 0
 
     def _window_for(self, n: int) -> int:
@@ -293,13 +294,20 @@ class GpuSampler:
         """Next n specs of the stream as a device [n, 64] uint8 tensor; raises on stream failure lazily
         (call ``check()`` or read ``specs_host``)."""
         torch = N.require_cuda()
-        if out is None:
-            out = torch.empty((n, 64), dtype=torch.uint8, device="cuda")
+        st = stream if stream is not None else torch.cuda.current_stream()
         window = self._window_for(n)
         nbytes = C.c_int64(0)
         N.check(N.lib().pf_sample_workspace_bytes(C.byref(self.cfg), window, C.byref(nbytes)), "pf_sample_workspace_bytes")
-        if self._ws is None or self._ws.numel() < nbytes.value:
-            self._ws = torch.empty((nbytes.value,), dtype=torch.uint8, device="cuda")
+        # allocations belong to the stream the kernels run on: the caching allocator then never
+        # hands a block still in use by a side-stream sampler launch to another stream
+        with torch.cuda.stream(st):
+            if out is None:
+                out = torch.empty((n, 64), dtype=torch.uint8, device="cuda")
+            if self._ws is None or self._ws.numel() < nbytes.value:
+                self._ws = torch.empty((nbytes.value,), dtype=torch.uint8, device="cuda")
+                self._ws_stream = st
+        if st != self._ws_stream:  # used off its allocation stream: keep it alive past this launch
+            self._ws.record_stream(st)
         N.check(
             N.lib().pf_sample(C.byref(self.cfg), self.slides_dev.data_ptr(), self.descs_dev.data_ptr(),
                               self.state.data_ptr(), n, out.data_ptr(), self._ws.data_ptr(), nbytes.value, window,
@@ -387,14 +395,16 @@ class CappedSampler:
 
     def next_batch(self, n: int, out=None, stream=None):
         torch = N.require_cuda()
+        st = stream if stream is not None else torch.cuda.current_stream()
         if out is None:
-            out = torch.empty((n, 64), dtype=torch.uint8, device="cuda")
+            with torch.cuda.stream(st):
+                out = torch.empty((n, 64), dtype=torch.uint8, device="cuda")
         k = min(n, self.cap - self.n_stored)
-        if k > 0:  # pass-through and retain
-            fresh = self.sampler.next_batch(k, stream=stream)
-            with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
-                self.stored[self.n_stored:self.n_stored + k].copy_(fresh)
-                out[:k].copy_(fresh)
+        if k > 0:  # pass-through and retain: sampled straight into the retained range (no temporary)
+            kept = self.stored[self.n_stored:self.n_stored + k]
+            self.sampler.next_batch(k, out=kept, stream=st)
+            with torch.cuda.stream(st):
+                out[:k].copy_(kept)
             self.n_stored += k
         if n - k > 0:
             N.check(N.lib().pf_capped_draw(self.key, self.counter.data_ptr(), self.stored.data_ptr(), self.n_stored,

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import json
 import math
+import weakref
 from dataclasses import dataclass, field
 from pathlib import Path
 
@@ -170,7 +171,15 @@ class GpuSlide:
         self.tile_maps = [None] * len(levels)  # int32 [ty * tx] slot map for compacted levels
         self.resident = [None] * len(levels)  # host bool [ty, tx] of compacted levels
         self.factor = factor
+        # fault word of the descriptor (pf_slide_desc.status_word): a read of a non-resident tile
+        # of a compacted level sets it; check_status() raises OutOfBoundsError
+        self.status = None
+        if levels:
+            import torch
+
+            self.status = torch.zeros(1, dtype=torch.int32, device=levels[0].device)
         self.desc = self._make_desc()
+        self._sets = weakref.WeakSet()  # SlideSets holding a device copy of self.desc
 
     def compact(self, plan) -> None:
         """Keep only the planned tiles resident (residency.reachable_tiles): each level becomes
@@ -178,6 +187,8 @@ class GpuSlide:
         freed.  Reads of non-resident tiles return zeros (pf_slide_desc.tile_map)."""
         torch = N.require_cuda()
         T = self.record.tile_size
+        # in-flight reads (any stream) of the dense levels finish before they are freed
+        torch.cuda.synchronize()
         for li, keep in enumerate(plan):
             if self.tile_maps[li] is not None:
                 raise ValueError(f"level {li} is already compacted")
@@ -200,6 +211,10 @@ class GpuSlide:
             self.resident[li] = keep
         self.desc = self._make_desc()
         self._own_set = None
+        # every SlideSet built earlier (and the samplers / loaders sharing its descriptor tensor)
+        # sees the new level pointers and slot maps: no read can reach the freed dense levels
+        for ss in list(self._sets):
+            ss._refresh(self)
 
     @property
     def compacted(self) -> bool:
@@ -318,7 +333,30 @@ class GpuSlide:
         d.n_levels = len(rec.levels)
         d.tile_size = rec.tile_size
         d.base_mpp = rec.base_mpp
+        d.status_word = int(self.status.data_ptr()) if getattr(self, "status", None) is not None else 0
         return d
+
+    def require_resident(self, spec) -> None:
+        """Host check of a planned spec (plan_specs row) against a compacted level: the window
+        must lie on resident tiles, else OutOfBoundsError (the device path would read the hole)."""
+        li = int(spec["level"])
+        if self.resident[li] is None:
+            return
+        lv, T = self.record.levels[li], self.record.tile_size
+        x0, y0, side = int(spec["sx"]), int(spec["sy"]), int(spec["side"])
+        tx0, ty0 = max(x0, 0) // T, max(y0, 0) // T
+        tx1, ty1 = min(x0 + side - 1, lv.width - 1) // T, min(y0 + side - 1, lv.height - 1) // T
+        if not self.resident[li][ty0:ty1 + 1, tx0:tx1 + 1].all():
+            raise OutOfBoundsError(f"region {(int(spec['x']), int(spec['y']), int(spec['width']), int(spec['height']))} "
+                                   "reads tiles that are not HBM-resident (slide compacted to the sampler's "
+                                   "reachable tiles)")
+
+    def check_status(self, stream=None, clear: bool = True) -> None:
+        """Raise OutOfBoundsError if a device read since the last check reached a non-resident tile
+        (pf_slide_status; synchronises the stream)."""
+        rc = N.lib().pf_slide_status(self.desc, 1 if clear else 0, N.stream_ptr(stream))
+        if rc != N.PF_OK:
+            N.check(rc, f"slide {self.record.slide_id!r}")
 
     # -- reads ------------------------------------------------------------
     def select_level(self, target_mpp: float) -> int:
@@ -351,20 +389,12 @@ class GpuSlide:
     def read_region(self, rect_level0, target_mpp: float, out_size: int) -> np.ndarray:
         """Drop-in Slide.read_region (pkg/store.py:651-688): (out, out, 3) uint8 host array."""
         specs = plan_specs([(0, rect_level0, target_mpp, out_size)], [self.record])
-        li = int(specs[0]["level"])
-        if self.resident[li] is not None:  # compacted level: the window must lie on resident tiles
-            lv, T = self.record.levels[li], self.record.tile_size
-            x0 = round_half_away(rect_level0[0] / lv.downsample)
-            y0 = round_half_away(rect_level0[1] / lv.downsample)
-            side = int(specs[0]["side"])
-            tx0, ty0 = max(x0, 0) // T, max(y0, 0) // T
-            tx1, ty1 = min(x0 + side - 1, lv.width - 1) // T, min(y0 + side - 1, lv.height - 1) // T
-            if not self.resident[li][ty0:ty1 + 1, tx0:tx1 + 1].all():
-                raise StoreError(f"region {tuple(rect_level0)} reads tiles that are not HBM-resident "
-                                 "(slide compacted to the sampler's reachable tiles)")
+        self.require_resident(specs[0])
         if getattr(self, "_own_set", None) is None:
             self._own_set = SlideSet([self])
         out = self._own_set.read_regions(specs, out_size)
+        if self.compacted:
+            self.check_status()
         return out[0].cpu().numpy()
 
 
@@ -638,10 +668,43 @@ def plan_specs(requests, records) -> np.ndarray:
         sx, sy = round_half_away(x / lv.downsample), round_half_away(y / lv.downsample)
         if sx < -1 or sy < -1 or sx + side > lv.width + 1 or sy + side > lv.height + 1:
             raise OutOfBoundsError(f"window ({sx}, {sy}, {side}, {side}) outside level {li} ({lv.width}x{lv.height})")
-        if side != out_size and 2 * math.ceil(max(side / out_size, 1.0)) + 1 > 32:
-            raise ValueError(f"down-ratio {side}/{out_size} too large for the resampler")
         specs[i] = (i, mpp, si, x, y, w, h, out_size, -1, li, side, sx, sy, 0)
     return specs
+
+
+_FITS: dict = {}
+
+
+def _generic_indices(specs, out_size: int, dtype_code: int) -> list:
+    """Indices of host specs whose window pf_read_regions' fused kernel cannot stage."""
+    arr = np.asarray(specs)
+    out = []
+    for i, side in enumerate(arr["side"].tolist()):
+        key = (int(side), int(out_size), int(dtype_code))
+        if key not in _FITS:
+            f = N.C.c_int32(0)
+            N.check(N.lib().pf_read_region_fits(key[0], key[1], key[2], N.C.byref(f)), "pf_read_region_fits")
+            _FITS[key] = bool(f.value)
+        if not _FITS[key]:
+            out.append(i)
+    return out
+
+
+def _read_generic(descs, spec, out_size, code, lay, m, s, out, stream):
+    """pf_read_region_generic for one host spec (level/side/sx/sy planned) into `out` (one patch)."""
+    import torch
+
+    st = stream if stream is not None else torch.cuda.current_stream()
+    rec = np.ascontiguousarray(np.asarray(spec, dtype=N.SPEC_DTYPE).reshape(1))
+    need = N.C.c_int64(0)
+    N.check(N.lib().pf_read_region_generic_scratch_bytes(int(rec["side"][0]), out_size, N.C.byref(need)),
+            "pf_read_region_generic_scratch_bytes")
+    with torch.cuda.stream(st):
+        scratch = torch.empty((max(1, need.value),), dtype=torch.uint8, device="cuda")
+    N.check(N.lib().pf_read_region_generic(descs.data_ptr(), rec.ctypes.data, out_size, code, lay,
+                                           N.C.cast(m, N.C.c_void_p), N.C.cast(s, N.C.c_void_p),
+                                           scratch.data_ptr(), need.value, out.data_ptr(), N.stream_ptr(st)),
+            "pf_read_region_generic")
 
 
 class SlideSet:
@@ -656,6 +719,25 @@ class SlideSet:
         self.index = {sid: i for i, sid in enumerate(self.ids)}
         raw = b"".join(bytes(s.desc) for s in self.slides)
         self.descs = torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
+        for s in self.slides:
+            if hasattr(s, "_sets"):
+                s._sets.add(self)
+
+    def check_status(self, stream=None) -> None:
+        """OutOfBoundsError if any device read since the last check hit a non-resident tile."""
+        for s in self.slides:
+            if getattr(s, "compacted", False):
+                s.check_status(stream)
+
+    def _refresh(self, slide) -> None:
+        """Rewrite the device descriptor of ``slide`` in place (GpuSlide.compact)."""
+        import torch
+
+        d = bytes(slide.desc)
+        for i, s in enumerate(self.slides):
+            if s is slide:
+                self.descs[i * len(d):(i + 1) * len(d)].copy_(torch.frombuffer(bytearray(d), dtype=torch.uint8))
+        torch.cuda.synchronize()
 
     def __len__(self):
         return len(self.slides)
@@ -689,10 +771,23 @@ class SlideSet:
         if out is None:
             out = torch.empty(shape, dtype=tdt, device="cuda")
         sp = N.stream_ptr(stream)
-        if not planned:
-            N.check(N.lib().pf_plan_regions(self.descs.data_ptr(), dspecs.data_ptr(), n, sp), "pf_plan_regions")
         m = (N.C.c_float * 3)(*mean)
         s = (N.C.c_float * 3)(*std)
+        big = [] if isinstance(specs, torch.Tensor) else _generic_indices(specs, out_size, code)
+        if big:  # windows the fused kernel cannot stage: one generic PIL read each (rare)
+            host = np.ascontiguousarray(specs, dtype=N.SPEC_DTYPE)
+            keep = np.ones(n, dtype=bool)
+            keep[big] = False
+            for i in big:
+                _read_generic(self.descs, host[i], out_size, code, lay, m, s, out[i], stream)
+            if keep.any():
+                idx = np.flatnonzero(keep)
+                sub = self.read_regions(host[idx], out_size, dtype=dtype, layout=layout, mean=mean, std=std,
+                                        stream=stream, planned=planned)
+                out[torch.from_numpy(idx).to(out.device)] = sub
+            return out
+        if not planned:
+            N.check(N.lib().pf_plan_regions(self.descs.data_ptr(), dspecs.data_ptr(), n, sp), "pf_plan_regions")
         N.check(
             N.lib().pf_read_regions(self.descs.data_ptr(), dspecs.data_ptr(), n, out_size, code, lay,
                                     N.C.cast(m, N.C.c_void_p), N.C.cast(s, N.C.c_void_p), out.data_ptr(), sp),
