@@ -200,8 +200,10 @@ def build_slides(args, rank, world):
 class Feed:
     """One benchmark workload: a loader plus what the roofline needs to know about it."""
 
-    def __init__(self, loader, stage: str, bytes_per_patch: int, kernel: str, workload: str, e2e_fn):
-        self.loader, self.stage, self.bytes_per_patch = loader, stage, bytes_per_patch
+    def __init__(self, loader, stage, bytes_per_patch: int, kernel: str, workload: str, e2e_fn):
+        # stage: the timed stage(s) whose summed time is the roofline's per-step kernel time
+        self.loader, self.stages, self.bytes_per_patch = loader, (stage,) if isinstance(stage, str) else tuple(stage), \
+            bytes_per_patch
         self.kernel, self.workload, self.e2e_fn = kernel, workload, e2e_fn
 
     @property
@@ -241,6 +243,12 @@ def make_feed(args, pf, plan, slides, rank, src_size=224, n_local=8, patch=224):
     else:
         wl = (f"{tag}: {args.slides} slides {args.width}x{args.height} per GPU in HBM, sat>0.07+morph mask on 1/32 "
               f"thumbnail, epoch_stream sampler 224px min_fg 0.40, DINOv2 multi-crop 2x224 + {n_local}x96 {args.dtype} NCHW")
+    if args.config == "3":  # E[source] over mpp U{0.25, 0.5, 1, 2}: 224^2, 448^2 (L0), 224^2, 448^2 (L1) u8
+        src = (224 * 224 + 448 * 448 + 224 * 224 + 448 * 448) * 3 // 4
+        bpp = mc.bytes_per_patch(args.dtype) - 3 * mc.src_size ** 2 + src
+        return Feed(loader, ("resample", "multicrop"), bpp,
+                    "read_regions_kernel (PIL 448->224, half the patches) + multicrop_kernel (both launches)", wl,
+                    run_e2e_multicrop)
     return Feed(loader, "multicrop", mc.bytes_per_patch(args.dtype), "multicrop_kernel (global + local crop launches)",
                 wl, run_e2e_multicrop)
 
@@ -396,7 +404,7 @@ def result_line(feed, args, world, elapsed_ms, stage_ms, launches, clocks, st, e
     peak, peak_kind = measured_peak_hbm()
     n_total = args.steps * args.batch * world
     value = n_total / (elapsed_ms / 1000.0)
-    k_ms = stage_ms[feed.stage]
+    k_ms = sum(stage_ms[k] for k in feed.stages)
     achieved = feed.bytes_per_patch * args.batch / (k_ms / 1000.0) / 1e9
     traffic = None
     tp = ROOT / "profiles" / f"traffic_config{args.config}.json"
@@ -492,7 +500,7 @@ def run_b200(args):
             e2e["value"] = round(world * n_rank / float(te.item()), 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, steps=args.cpu_steps)
+        cpu = cpu_baseline(args, steps=args.cpu_steps, slides=slides)
     if rank == 0:
         print(json.dumps(result_line(feed, args, world, elapsed_ms, stage_ms, launches, clocks, st, e2e, cpu)), flush=True)
     if world > 1:
@@ -535,38 +543,60 @@ def run_sweep(args, pf, plan, slides, rank, world, local, torch, dist, N):
 # CPU arms (oracle port on the host cores)
 
 
-def cpu_baseline(args, steps=2):
+def _cpu_polygons(args, slides=None):
+    """Rings for the CPU arm: the GPU arm's traced saturation+morphology polygons when this process
+    built them (same_config), else the committed masks of the 16 C2 slides (tests/golden/
+    c2_masks16.npz, made by the GPU arm's renderer and mask kernel) traced by the oracle, else
+    the synthetic field's mask."""
+    if slides is not None:
+        return [[np.asarray(r) for r in poly.rings] for _, poly in slides], "gpu_arm"
+    p = ROOT / "tests" / "golden" / "c2_masks16.npz"
+    if args.config in ("2", "3") and (args.width, args.height) == (40000, 30000) and args.slides <= 16 and p.exists():
+        from oracle import port
+
+        z = np.load(p)
+        polys = []
+        for g in range(args.slides):
+            shape = tuple(z[f"s{g}_shape"])
+            bits = np.unpackbits(z[f"s{g}_mask"])[: shape[0] * shape[1]].reshape(shape).astype(bool)
+            polys.append(port.polygon_from_mask(bits, float(z[f"s{g}_scale"][0]), 64.0))
+        return polys, "c2_masks16"
+    return None, "field"
+
+
+def _cpu_run(args, steps, polygons):
     from oracle import cpu_pipeline as cp
 
     cores = cp.cpu_count()
     if args.config == "4":  # the C4 set's sizes come from a seed; the CPU sample uses its mean slide
         args.width, args.height = 70000, 55000
-    per_step, cands = cp.run(cores, args.slides, args.width, args.height, candidates_per_step=1, steps=steps + 1,
-                             augment=args.config != "1")
+    per_step, cands = cp.run(cores, args.slides, args.width, args.height, candidates_per_step=1, steps=steps,
+                             augment=args.config != "1", polygons=polygons)
+    return cp, cores, per_step, cands
+
+
+def cpu_baseline(args, steps=2, slides=None):
+    polygons, poly_src = _cpu_polygons(args, slides)
+    cp, cores, per_step, cands = _cpu_run(args, steps + 1, polygons)
     timed = per_step[1:]
-    t = sum(d for d, _ in timed)
-    n = sum(m for _, m in timed)
-    return {"value": round(n / t, 4) if t > 0 else 0.0, "unit": "patches/s", "cores": cores, "kind": "port",
-            "sample": f"{steps} steps x {cores} workers x 1 epoch_stream candidate each (+ read_region + "
-                      f"{'torchvision multi-crop' if args.config != '1' else 'normalize_patch'} of accepted specs); "
-                      f"{n} patches in {t:.1f} s; {cands} candidates total"}
+    value, stages = cp.summarize(timed, cores, cands, augment=args.config != "1")
+    return {"value": round(value, 4), "unit": "patches/s", "cores": cores, "kind": "port",
+            "cpu_model": cp.cpu_model(), "stages": stages, "polygons": poly_src,
+            "same_config": poly_src in ("gpu_arm", "c2_masks16"),
+            "sample": f"{steps} steps x {cores} workers: 1 epoch_stream candidate, 48 read_region+normalize_patch, "
+                      f"4 torchvision multi-crops each; value = 1/(1/sampler + 1/loader + 1/augment) "
+                      f"over all workers; {cands} candidates total"}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle import cpu_pipeline as cp
-
-    cores = cp.cpu_count()
-    if args.config == "4":  # the C4 set's sizes come from a seed; the CPU sample uses its mean slide
-        args.width, args.height = 70000, 55000
-    per_step, cands = cp.run(cores, args.slides, args.width, args.height, candidates_per_step=1,
-                             steps=args.warmup + args.steps, augment=args.config != "1")
+    polygons, poly_src = _cpu_polygons(args)
+    cp, cores, per_step, cands = _cpu_run(args, args.warmup + args.steps, polygons)
     timed = per_step[args.warmup:]
-    t = sum(d for d, _ in timed)
-    n = sum(m for _, m in timed)
-    value = n / t if t > 0 else 0.0
+    value, stages = cp.summarize(timed, cores, cands, augment=args.config != "1")
+    t = sum(max(s["sampler"][0], 0) + s["loader"][0] + s["augment"][0] for s in timed)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -582,13 +612,15 @@ def run_reference(args):
         "dtype": args.dtype,
         "data": "synthetic (numpy restatement of the same generator, tiles rendered on first touch)",
         "config": {"workload": f"C{args.config} on CPU: {args.slides} slides {args.width}x{args.height}, reference "
-                               "epoch_stream (numpy even-odd overlap), read_region, " +
-                               ("normalize_patch (ImageNet) fp32" if args.config == "1" else
+                               "epoch_stream (numpy even-odd overlap), read_region + normalize_patch, " +
+                               ("(no augmentation)" if args.config == "1" else
                                 "torchvision multi-crop 2x224+8x96, bf16"),
                    "global_batch": args.batch, "parallelism": f"{cores} worker processes, seed + worker"},
         "cpu_baseline": {"value": round(value, 4), "unit": "patches/s", "cores": cores, "kind": "port",
-                         "sample": f"{len(timed)} steps x {cores} workers x 1 sampler candidate; {n} patches, "
-                                   f"{cands} candidates"},
+                         "cpu_model": cp.cpu_model(), "stages": stages, "polygons": poly_src,
+                         "same_config": poly_src in ("gpu_arm", "c2_masks16"),
+                         "sample": f"{len(timed)} steps x {cores} workers: 1 sampler candidate, 48 loads, 4 "
+                                   f"multi-crops each; {cands} candidates"},
         "e2e": {"value": round(value, 4), "unit": "patches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

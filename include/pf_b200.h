@@ -228,6 +228,21 @@ int pf_polygon_trace(const uint8_t* mask, int32_t h, int32_t w, double scale, do
                      double* xy, int64_t xy_cap_points, int64_t* ring_off, int32_t ring_cap,
                      int64_t* n_points, int32_t* n_rings);
 
+/* polygon_from_mask on the GPU: the same rings as
+ * pf_polygon_trace, ring for ring and vertex for vertex, from a DEVICE mask
+ * (h, w) uint8 (e.g. pf_mask's output) into DEVICE outputs (xy: n_points
+ * (x, y) float64 pairs, ring_off: n_rings + 1 int64 offsets).  Segments are
+ * assembled into rings by pointer jumping (cycle first/last segment, list
+ * ranking) instead of find_contours' sequential joining.  `scratch` of
+ * pf_polygon_trace_device_scratch_bytes.  Synchronises `stream` (the ring and
+ * point counts size the outputs); PF_ERR_CAPACITY with *n_points/*n_rings set
+ * when the outputs are too small, PF_ERR_EMPTY_FOREGROUND as the reference. */
+int pf_polygon_trace_device_scratch_bytes(int32_t h, int32_t w, int64_t* bytes);
+int pf_polygon_trace_device(const uint8_t* mask_dev, int32_t h, int32_t w, double scale, double min_region_px,
+                            void* scratch, int64_t scratch_bytes, double* xy_dev, int64_t xy_cap_points,
+                            int64_t* ring_off_dev, int32_t ring_cap, int64_t* n_points, int32_t* n_rings,
+                            void* stream);
+
 /* Slab index of a ForegroundPolygon for the device even-odd test.  HOST
  * buffers: rings as concatenated (x, y) float64 with ring_off[n_rings+1].
  * _size reports the blob size; _build fills it (copy it to the device as is). */

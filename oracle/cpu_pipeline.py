@@ -188,8 +188,11 @@ def augment_patch(src, rs, mean, std):
 
 
 def _worker_main(args):
-    """Process worker: build its slides, then run `candidates` sampler attempts + read + augment per step."""
-    (wid, seed, n_slides, width, height, candidates, steps, mean, std, q, polys, augment) = args
+    """Process worker: build its slides, then per step time the three stages BASELINE.md §4 asks for:
+    sampler (`candidates` epoch_stream attempts), loader (read_region + normalize_patch over a
+    manifest of `loads` rects, `patchforge load` semantics) and augmentation (torchvision multi-crop
+    of `augs` patches, not reference code)."""
+    (wid, seed, n_slides, width, height, candidates, steps, mean, std, q, polys, augment, loads, augs) = args
     import torch
 
     torch.set_num_threads(1)
@@ -197,22 +200,34 @@ def _worker_main(args):
     augment_patch(np.zeros((224, 224, 3), np.uint8), np.random.default_rng(0), mean, std)  # warm imports
     w = Worker(slides, polys, seed + wid)
     rs = np.random.default_rng(seed + wid)
-    q.put(("ready", wid, 0, 0.0, 0))
+    q.put(("ready", wid, 0, None, 0))
     for step in range(steps):
+        # sampler
         t0 = time.perf_counter()
         made = 0
         for _ in range(candidates):
-            spec = w.candidate()
-            if spec is not None:
-                si, x, y = spec
-                px = slides[si].read_region224(x, y)
-                if augment:
-                    augment_patch(px, rs, mean, std)
-                else:  # config 1: normalize_patch with ImageNet mean/std, NCHW fp32
-                    np.ascontiguousarray(port.normalize_patch(px, mean, std).transpose(2, 0, 1))
+            if w.candidate() is not None:
                 made += 1
-        q.put(("step", wid, step, time.perf_counter() - t0, made))
-    q.put(("done", wid, 0, 0.0, w.candidates))
+        ts = time.perf_counter() - t0
+        # loader over a pre-sampled manifest (uniform level-0 rects: read cost does not depend on them)
+        man = [(int(rs.integers(n_slides)), int(rs.integers(0, width - 224)), int(rs.integers(0, height - 224)))
+               for _ in range(loads)]
+        t0 = time.perf_counter()
+        pix = []
+        for si, x, y in man:
+            px = slides[si].read_region224(x, y)
+            np.ascontiguousarray(port.normalize_patch(px, mean, std).transpose(2, 0, 1))
+            pix.append(px)
+        tl = time.perf_counter() - t0
+        # augmentation (config 1 has none)
+        ta = 0.0
+        if augment:
+            t0 = time.perf_counter()
+            for px in pix[:augs]:
+                augment_patch(px, rs, mean, std)
+            ta = time.perf_counter() - t0
+        q.put(("step", wid, step, (ts, made, tl, len(man), ta, min(augs, len(pix)) if augment else 0), 0))
+    q.put(("done", wid, 0, None, w.candidates))
 
 
 def _slide_polygon(a):
@@ -221,16 +236,23 @@ def _slide_polygon(a):
 
 
 def run(n_workers, n_slides, width, height, candidates_per_step, steps, seed=0, mean=(0.485, 0.456, 0.406),
-        std=(0.229, 0.224, 0.225), augment=True):
-    """Yields per-step (wall_seconds, patches) aggregated over the worker pool."""
+        std=(0.229, 0.224, 0.225), augment=True, loads_per_step=48, augs_per_step=4, polygons=None):
+    """Per-step stage timings aggregated over the worker pool.  Returns (steps, total candidates),
+    each step a dict: sampler (seconds, accepted), loader (seconds, patches), augment (seconds,
+    patches) -- the max over workers of each stage's time and the sum of its units.
+    ``polygons``: rings per slide (e.g. the GPU arm's traced polygons); default: the field mask."""
     import multiprocessing as mp
 
     ctx = mp.get_context("spawn")
-    with ctx.Pool(min(n_workers, n_slides)) as pool:
-        polys = pool.map(_slide_polygon, [(width, height, 1000 + i) for i in range(n_slides)])
+    if polygons is None:
+        with ctx.Pool(min(n_workers, n_slides)) as pool:
+            polys = pool.map(_slide_polygon, [(width, height, 1000 + i) for i in range(n_slides)])
+    else:
+        polys = [[np.asarray(r, dtype=np.float64) for r in p] for p in polygons]
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker_main, args=((i, seed, n_slides, width, height, candidates_per_step, steps, mean,
-                                                    std, q, polys, augment),)) for i in range(n_workers)]
+                                                    std, q, polys, augment, loads_per_step, augs_per_step),))
+             for i in range(n_workers)]
     for p in procs:
         p.start()
     ready = 0
@@ -241,16 +263,54 @@ def run(n_workers, n_slides, width, height, candidates_per_step, steps, seed=0, 
     done = 0
     total_cands = 0
     while done < n_workers:
-        kind, wid, step, dt, made = q.get()
+        kind, wid, step, st, made = q.get()
         if kind == "step":
-            t, m = per_step.get(step, (0.0, 0))
-            per_step[step] = (max(t, dt), m + made)
+            ts, acc, tl, nl, ta, na = st
+            agg = per_step.setdefault(step, {"sampler": [0.0, 0], "loader": [0.0, 0], "augment": [0.0, 0]})
+            for k, (t, m) in (("sampler", (ts, acc)), ("loader", (tl, nl)), ("augment", (ta, na))):
+                agg[k][0] = max(agg[k][0], t)
+                agg[k][1] += m
         elif kind == "done":
             done += 1
             total_cands += made
     for p in procs:
         p.join()
     return [per_step[s] for s in sorted(per_step)], total_cands
+
+
+def summarize(steps, cores, candidates, augment=True):
+    """Stage rates (patches/s over all workers) and the end-to-end rate of a worker running the three
+    stages per patch: 1 / (1/sampler + 1/loader + 1/augment)."""
+    def rate(k):
+        t = sum(s[k][0] for s in steps)
+        n = sum(s[k][1] for s in steps)
+        return (n / t if t > 0 else 0.0), n, t
+
+    rs, ns, tsam = rate("sampler")
+    rl, nl, tl = rate("loader")
+    ra, na, ta = rate("augment") if augment else (float("inf"), 0, 0.0)
+    inv = (1.0 / rs if rs > 0 else float("inf")) + 1.0 / rl + (1.0 / ra if augment else 0.0)
+    e2e = 1.0 / inv if inv < float("inf") else 0.0
+    stages = {"sampler": {"value": round(rs, 4), "unit": "specs/s", "specs": ns, "seconds": round(tsam, 2),
+                          "what": "reference epoch_stream attempts (numpy even-odd overlap, 128x128 lattice)"},
+              "loader": {"value": round(rl, 1), "unit": "patches/s", "patches": nl, "seconds": round(tl, 2),
+                         "what": "read_region 224 passthrough + normalize_patch over a manifest (patchforge load)"}}
+    if augment:
+        stages["augment"] = {"value": round(ra, 2), "unit": "patches/s", "patches": na, "seconds": round(ta, 2),
+                             "what": "torchvision v2 multi-crop 2x224+8x96 bf16 (NOT reference code)"}
+    return e2e, stages
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def cpu_count():

@@ -29,6 +29,7 @@ from .foreground import (
     overlap_fraction,
     overlap_fractions,
     polygon_from_mask,
+    polygon_from_mask_device,
     rect_polygon,
 )
 from .pipeline import (

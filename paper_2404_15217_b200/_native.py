@@ -199,6 +199,9 @@ class _Lib:
                 [vp, i32, i32, dbl, dbl, vp, i64, vp, i32, C.POINTER(i64), C.POINTER(i32)],
                 C.c_int,
             ),
+            "pf_polygon_trace_device_scratch_bytes": ([i32, i32, C.POINTER(i64)], C.c_int),
+            "pf_polygon_trace_device": (
+                [vp, i32, i32, dbl, dbl, vp, i64, vp, i64, vp, i32, C.POINTER(i64), C.POINTER(i32), vp], C.c_int),
             "pf_polygon_index_size": ([vp, vp, i32, C.POINTER(i64)], C.c_int),
             "pf_polygon_index_build": ([vp, vp, i32, vp, i64], C.c_int),
             "pf_overlap_fraction": ([vp, vp, i32, i32, vp, vp], C.c_int),

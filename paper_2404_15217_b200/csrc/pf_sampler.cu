@@ -261,8 +261,15 @@ __device__ inline int slow_attempt(const pf_sampler_config& cfg, const pf_sample
 // against the accept bitmaps staged in shared memory; each emitted spec is
 // recorded as (slide, window offset) and materialised afterwards by the whole
 // block.  The exact sequential path finishes whatever the table cannot decide.
-constexpr int kWalkThreads = 256;
+constexpr int kWalkThreads = 512;
 constexpr int kDrawCache = 256;
+constexpr int kFastDraws = 8192;  // slide draws precomputed per fast walk (int16 in shared memory)
+
+__device__ inline double k_total_weight(const pf_sampler_config& cfg, const pf_sampler_slide* slides) {
+    double total = 0.0;
+    for (int k = 0; k < cfg.n_slides; ++k) total = __dadd_rn(total, slides[k].weight);
+    return total;
+}
 
 __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
     pf_sampler_config cfg, const pf_sampler_slide* slides, const pf_slide_desc* descs, pf_sampler_state* state,
@@ -316,8 +323,9 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                 }
             }
             __syncthreads();
-            for (int i = tid; i < cfg.n_slides * window; i += kWalkThreads) {
-                const int sl = i / window, a = i - sl * window;
+            for (int sl = 0; sl < cfg.n_slides; ++sl)
+            for (int a = tid; a < window; a += kWalkThreads) {
+                const int i = sl * window + a;
                 const uint32_t* bm = bm_all + (size_t)sl * words;
                 const int wd = a >> 5;
                 const uint32_t m = bm[wd] & (0xffffffffu << (a & 31));
@@ -332,7 +340,110 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
             }
             __syncthreads();
         }
-        if (tid < 32) {
+        // fast walk: every slide draw of the call precomputed in parallel (no rejected draw among
+        // them), then one thread runs the chain a -> next_accept(slide_j, a) + 1 whose only
+        // dependent load per draw is the next-accept table; bookkeeping is off the chain
+        int16_t* fdraw = reinterpret_cast<int16_t*>(na + (size_t)cfg.n_slides * window);
+        __shared__ int s_fast;
+        int n_fd = 0;
+        if (next_table) {
+            n_fd = min(kFastDraws, 2 * (n - w.emitted) + 256);
+            if (tid == 0) s_fast = 1;
+            __syncthreads();
+            for (int i = tid; i < n_fd; i += kWalkThreads) {
+                const uint64_t v = stream_u64(cfg.key_slide, w.c_slide + 1 + (uint64_t)i);
+                int sidx;
+                if (cfg.strategy == 0) {
+                    const uint64_t nn = (uint64_t)cfg.n_slides;
+                    sidx = randrange_accepts(v, randrange_limit(nn)) ? (int)(v % nn) : -1;
+                } else {
+                    const double u = __dadd_rn(0.0, __dmul_rn(u64_to_unit(v), __dsub_rn(k_total_weight(cfg, slides), 0.0)));
+                    double acc = 0.0;
+                    sidx = cfg.n_slides - 1;
+                    for (int k = 0; k < cfg.n_slides; ++k) {
+                        acc = __dadd_rn(acc, slides[k].weight);
+                        if (u < acc) {
+                            sidx = k;
+                            break;
+                        }
+                    }
+                }
+                if (sidx < 0) s_fast = 0;  // a rejected draw (p ~ n / 2^64): the general walk handles it
+                fdraw[i] = (int16_t)sidx;
+            }
+            __syncthreads();
+        }
+        if (next_table && s_fast) {
+            if (tid == 0) {
+                const uint64_t m0 = w.c_mpp;
+                const int wlim = min(window, *ws.reject_at);
+                int a = 0, j = 0, emitted = w.emitted, used = 0;
+                int64_t failures = w.failures;
+                int status = w.status;
+                bool mid_draw = false;
+                // the draw in hand (s, its table row, attempts it already used) and the next one,
+                // loaded ahead so the chain per draw is one table load + compare
+                int s = w.cur_slide;
+                if (s >= 0) {
+                    used = w.cur_used;
+                } else if (n_fd > 0) {
+                    s = fdraw[0];
+                    j = 1;
+                }
+                int s_nxt = j < n_fd ? fdraw[j] : 0;
+                const uint16_t* row = na + (size_t)max(s, 0) * window;
+                while (s >= 0 && emitted < n && status == PF_OK) {
+                    const int budget = max_att - used;
+                    if (a >= wlim) {  // the window ends at this draw's first attempt
+                        mid_draw = true;
+                        break;
+                    }
+                    const int f = row[a];
+                    if (f < min(a + budget, wlim)) {  // accepted: one spec, the draw is done
+                        emit_list[emitted - s_first] = make_int2(s, f);
+                        ++emitted;
+                        a = f + 1;
+                        failures = 0;
+                    } else if (a + budget <= wlim) {  // ExhaustedAttemptsError: redraw, no seq consumed
+                        a += budget;
+                        if (++failures >= flimit) status = PF_ERR_NO_SAMPLABLE;
+                    } else {  // the window (or a rejected coords draw) ends inside this draw
+                        used += wlim - a;
+                        a = wlim;
+                        mid_draw = true;
+                        break;
+                    }
+                    // next draw (only if the stream continues: no draw is taken past the n-th spec
+                    // or a NoSamplableSlideError)
+                    used = 0;
+                    if (emitted >= n || status != PF_OK || j == n_fd) {  // j == n_fd: the next round continues
+                        s = -1;
+                        break;
+                    }
+                    s = s_nxt;
+                    row = na + (size_t)s * window;
+                    ++j;
+                    s_nxt = fdraw[min(j, n_fd - 1)];
+                }
+                if (!mid_draw) used = 0;
+                w.c_slide += (uint64_t)j;
+                w.c_mpp = m0 + (uint64_t)a;
+                w.c_coords += 2ull * (uint64_t)a;
+                w.attempts += a;
+                w.seq += emitted - w.emitted;
+                w.emitted = emitted;
+                w.failures = failures;
+                w.status = status;
+                // a draw taken from the table but not finished stays current (cur_slide); a draw
+                // taken and finished is consumed; j counts the table entries taken
+                w.cur_slide = mid_draw ? s : -1;
+                w.cur_used = mid_draw ? used : 0;
+                s_last = emitted;
+                store_ws(state, w);
+            }
+            __syncthreads();
+            if (tid < 32) load_ws(state, w);
+        } else if (tid < 32) {
             const uint64_t m0 = w.c_mpp;
             const int wlim = min(window, *ws.reject_at);
             int draw_pos = kDrawCache, draw_cnt = kDrawCache;
@@ -560,7 +671,7 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     const int bm_in_smem = rounds > 0 && bm_bytes_all <= 160 * 1024;
     // next-accepted-offset table beside the bitmaps (uint16 offsets: window < 0xffff)
     const size_t nt_bytes = bm_bytes_all + ((size_t)cfg->n_slides * (window / 32) + 1) / 2 * 4 +
-                            (size_t)cfg->n_slides * window * 2;
+                            (size_t)cfg->n_slides * window * 2 + (size_t)kFastDraws * 2;
     const int next_table = bm_in_smem && window < 0xffff && nt_bytes <= 200 * 1024;
     const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid),
                                       next_table ? nt_bytes : (bm_in_smem ? bm_bytes_all : (size_t)0));

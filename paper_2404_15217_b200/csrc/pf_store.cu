@@ -145,10 +145,10 @@ __device__ __forceinline__ void write_out(void* out, int layout, int n_idx, int 
 //    tile pyramid with 16-byte cp.async (whole tile rows; clamped per-pixel
 //    gather only when the window touches the level edge), then written with
 //    the normalising epilogue (3x256 LUT) as 16-byte NCHW rows or HWC words;
-//  * resample (side != out): the band-0 CTA of the spec runs the PIL two-pass
-//    fixed-point resample for the whole patch (coefficients built in shared
-//    memory, source rows staged per band, horizontal pass into planar uint8,
-//    vertical pass straight into the epilogue); the other band CTAs exit.
+//  * resample (side != out): each band CTA runs the PIL two-pass fixed-point
+//    resample for its output rows (coefficients built in shared memory, the
+//    band's source rows staged in sub-bands, horizontal pass into planar uint8,
+//    vertical pass straight into the epilogue).
 constexpr int kRRThreads = 256;
 constexpr int kRRBand = 32;
 constexpr int kRRSmem = 96 * 1024;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
     const int side = sp.side;
     const bool pass = side == S;
     if (pass && skip_pass) return;
-    if (!pass && band > 0) return;
+    if (band * kRRBand >= S) return;
     OT* out = reinterpret_cast<OT*>(out_v);
     // LUT for the epilogue
     OT* lut = reinterpret_cast<OT*>(smem);
@@ -353,9 +353,12 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
     const int hplane = (cap + 4) * S;
     int R = (int)floor(((double)cap - 1.0 - 2.0 * ap.support) / ap.scale) + 1;
     R = R < 1 ? 1 : (R > S ? S : R);
-    const int nb = (S + R - 1) / R;
+    // this CTA's output rows: its kRRBand-row band of the patch (band-parallel across CTAs),
+    // resampled in internal bands of R rows that fit the staging ring
+    const int Yb0 = band * kRRBand, Yb1 = min(S, Yb0 + kRRBand);
+    const int nb = (Yb1 - Yb0 + R - 1) / R;
     auto rows_of = [&](int bnd, int& r0, int& r1) {  // axis_weights' own xmin / xmax bounds
-        const int y0 = bnd * R, y1 = min(S, y0 + R);
+        const int y0 = Yb0 + bnd * R, y1 = min(Yb1, y0 + R);
         r0 = (int)(ap.scale * ((double)y0 + 0.5) - ap.support + 0.5);
         r0 = r0 < 0 ? 0 : r0;
         r1 = (int)(ap.scale * ((double)(y1 - 1) + 0.5) + ap.support + 0.5);
@@ -392,7 +395,7 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
     };
     stage(0);
     for (int bnd = 0; bnd < nb; ++bnd) {
-        const int y0 = bnd * R, y1 = min(S, y0 + R);
+        const int y0 = Yb0 + bnd * R, y1 = min(Yb1, y0 + R);
         int r0, r1;
         rows_of(bnd, r0, r1);
         const int nr = r1 - r0;
@@ -619,9 +622,9 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
         np.mean[c] = mean3 ? mean3[c] : 0.5f;
         np.stdv[c] = std3 ? std3[c] : 0.5f;
     }
-    // passthrough specs split into row bands across CTAs; with PF_SKIP_PASSTHROUGH only the
-    // resampled specs do work (one CTA each), so no band CTAs are launched
-    const int n_bands = (layout & PF_SKIP_PASSTHROUGH) ? 1 : (out_size + kRRBand - 1) / kRRBand;
+    // every spec is split into kRRBand-row output bands across CTAs (passthrough and PIL resample
+    // alike); with PF_SKIP_PASSTHROUGH the passthrough specs' CTAs exit at once
+    const int n_bands = (out_size + kRRBand - 1) / kRRBand;
     const long long grid = (long long)n * n_bands;
     cudaStream_t st = as_stream(stream);
     int rc;

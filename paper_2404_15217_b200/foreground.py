@@ -206,6 +206,38 @@ def polygon_from_mask(mask: BinaryMask, min_region_px: float = DEFAULT_MIN_REGIO
     return ForegroundPolygon(rings, mask.scale, slide_id)
 
 
+def polygon_from_mask_device(mask, scale: float, min_region_px: float = DEFAULT_MIN_REGION_PX, slide_id: str = "",
+                             stream=None) -> ForegroundPolygon:
+    """polygon_from_mask (pkg/foreground.py:169-220) traced on the GPU (pf_polygon_trace_device):
+    ``mask`` is a (h, w) device tensor (e.g. mask_device's output), so the mask never leaves HBM.
+    The rings equal polygon_from_mask's on the same bits, vertex for vertex."""
+    torch = N.require_cuda()
+    if not isinstance(mask, torch.Tensor) or mask.dim() != 2:
+        raise ValueError("mask must be a (h, w) device tensor")
+    m = mask.to(device="cuda", dtype=torch.uint8).contiguous()
+    h, w = int(m.shape[0]), int(m.shape[1])
+    L = N.lib()
+    need = C.c_int64(0)
+    N.check(L.pf_polygon_trace_device_scratch_bytes(h, w, C.byref(need)), "pf_polygon_trace_device_scratch_bytes")
+    st = stream if stream is not None else torch.cuda.current_stream()
+    with torch.cuda.stream(st):
+        scratch = torch.empty((need.value,), dtype=torch.uint8, device="cuda")
+    npts, nr = C.c_int64(0), C.c_int32(0)
+    rc = L.pf_polygon_trace_device(m.data_ptr(), h, w, float(scale), float(min_region_px), scratch.data_ptr(),
+                                   need.value, None, 0, None, 0, C.byref(npts), C.byref(nr), N.stream_ptr(st))
+    if rc != N.PF_ERR_CAPACITY:
+        N.check(rc, "pf_polygon_trace_device")
+    with torch.cuda.stream(st):
+        xy = torch.empty((npts.value, 2), dtype=torch.float64, device="cuda")
+        off = torch.empty((nr.value + 1,), dtype=torch.int64, device="cuda")
+    N.check(L.pf_polygon_trace_device(m.data_ptr(), h, w, float(scale), float(min_region_px), scratch.data_ptr(),
+                                      need.value, xy.data_ptr(), npts.value, off.data_ptr(), nr.value + 1,
+                                      C.byref(npts), C.byref(nr), N.stream_ptr(st)), "pf_polygon_trace_device")
+    xy_h, off_h = xy.cpu().numpy(), off.cpu().numpy()
+    rings = [xy_h[off_h[i]:off_h[i + 1]].copy() for i in range(nr.value)]
+    return ForegroundPolygon(rings, scale, slide_id)
+
+
 def overlap_fractions(poly: ForegroundPolygon, rects, grid: int = OVERLAP_GRID, stream=None):
     """Batched overlap_fraction on device; rects (n, 4) (x, y, w, h) -> float64 device tensor."""
     torch = N.require_cuda()
