@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--device", type=int, default=None, help="CUDA device of every rank (default LOCAL_RANK)")
     ap.add_argument("--dump-dir", default=None, help="each rank writes its first batch's specs + crop params")
+    ap.add_argument("--tier-hbm-gb", type=float, default=None,
+                    help="config 4: level-0 tiles in a host-backed tier with this many GB of HBM slots per GPU "
+                         "(slide sets whose reachable tiles exceed HBM, e.g. --slides 32)")
     args = ap.parse_args()
     if args.mixed_mpp:
         args.config = "3"
@@ -161,6 +164,8 @@ def build_slides(args, rank, world):
     plan = rank_plan(rank, world, args.slides * world, seed=0)  # rank r owns slides [16r, 16r+16)
     slides = []
     resident, dense = 0, 0
+    tier_gb = getattr(args, "tier_hbm_gb", None)
+    tiered = []  # (slide, level-0 reachable plan) to move to the host-backed tier once all are built
     if args.config == "4":  # 128 slide sizes from one seed; rank r renders slides [16r, 16r + 16)
         rs = np.random.default_rng(4)
         dims = list(zip(rs.integers(40000, 100001, 128), rs.integers(30000, 80001, 128)))
@@ -189,10 +194,28 @@ def build_slides(args, rank, world):
             resident += R.resident_bytes(s.record, tiles)
             print(f"[rank {rank}] {sid} {w}x{h}: mask {bm.bits.mean():.3f}, pyramid {R.dense_bytes(s.record) / 1e9:.1f} GB"
                   f" -> {R.resident_bytes(s.record, tiles) / 1e9:.1f} GB resident", file=sys.stderr)
-            s.compact(tiles)
             import torch
 
+            if tier_gb:  # level 0 -> pinned host store now (HBM for the next render), slots sized later
+                from paper_2404_15217_b200 import tier as TR
+
+                n0 = int(tiles[0].sum())
+                st = TR.tier_level(s, 0, tiles[0], hbm_slots=1)
+                tiered.append((s, n0))
+                s.compact(tiles, levels=range(1, len(tiles)))
+            else:
+                s.compact(tiles)
             torch.cuda.empty_cache()
+    if tiered:  # HBM slot pools, split over the slides by reachable level-0 tiles
+        from paper_2404_15217_b200 import tier as TR
+
+        tb = 256 * 256 * 3
+        total = sum(n for _, n in tiered)
+        budget = int(tier_gb * 1e9 / tb)
+        for s, n in tiered:
+            TR.resize_pool(s, max(1, budget * n // total))
+        args.tier = {"reachable_l0_gb": round(total * tb / 1e9, 1), "hbm_slots_gb": round(budget * tb / 1e9, 1),
+                     "slides": len(tiered)}
     args.residency = {"dense_gb": round(dense / 1e9, 1), "resident_gb": round(resident / 1e9, 1)} if dense else None
     return pf, plan, slides
 
@@ -351,6 +374,8 @@ def timed_run(feed, args, torch, dist, world, local, N):
     for _ in range(max(args.warmup, 0)):
         loader.next_batch()
     torch.cuda.synchronize()
+    tiers = getattr(loader, "tiers", None)
+    filled0 = tiers.tiles_filled() if tiers is not None else 0
     loader.sampler.update_estimate()
     if world > 1:
         dist.barrier()
@@ -370,6 +395,10 @@ def timed_run(feed, args, torch, dist, world, local, N):
     torch.cuda.synchronize()
     clk.__exit__(None, None, None)
     launches = N.launches() - l0
+    if tiers is not None:  # host-backed tier traffic of the timed steps (zero-copy H2D by the fill kernel)
+        filled = tiers.tiles_filled() - filled0
+        args.tier_stats = {"tiles_filled_per_step": round(filled / args.steps, 1),
+                           "h2d_gb_per_step": round(filled * 256 * 256 * 3 / args.steps / 1e9, 3)}
     elapsed_ms = start.elapsed_time(end)
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda" if args.dist_backend == "nccl" else "cpu")
     if world > 1:
@@ -454,6 +483,9 @@ def result_line(feed, args, world, elapsed_ms, stage_ms, launches, clocks, st, e
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        **({"tier": {**args.tier, **getattr(args, "tier_stats", {}),
+                     "stall_ms_per_step": round(stage_ms.get("sample_wait", 0.0), 4)}}
+           if getattr(args, "tier", None) else {}),
     }
 
 

@@ -140,6 +140,41 @@ int pf_slide_build_pyramid(pf_slide* slide, void* stream);
 int pf_slide_status(const pf_slide_desc* desc_host, int32_t clear, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Host-backed tile tier (replaces TileCache/fetch_chunk,  */
+/* pkg/store.py:270-319, 611-649, for slide sets whose reachable tiles exceed */
+/* HBM).  A compacted level (tile_map != 0) gets a pool of n_slots HBM slots  */
+/* smaller than its reachable set, backed by a pinned device-mapped host copy */
+/* of every reachable tile.  All device addresses; one record per slide of    */
+/* the call (slot_owner == 0: the slide has no tier).                         */
+/* ------------------------------------------------------------------------ */
+typedef struct pf_tile_tier {
+    uint64_t host_tiles;    /* device address of the mapped host store (tile-major, T*T*3 per tile) */
+    uint64_t host_index;    /* int64[tiles_y * tiles_x]: tile -> index in the host store, -1 if absent */
+    uint64_t slot_owner;    /* int32[n_slots + 1]: tile held by each slot, -1 none */
+    uint64_t slot_last_use; /* int32[n_slots + 1]: last batch id that read the slot */
+    uint64_t requested;     /* int32[tiles]: request flags (all 0 between calls) */
+    uint64_t miss_list;     /* int32[max_miss] */
+    uint64_t victims;       /* int32[max_miss] */
+    uint64_t counters;      /* int32[8]: [0] misses, [1] filled (this batch), [2] clock hand, [4..5] u64 filled total */
+    int32_t level, n_slots, max_miss, _pad;
+} pf_tile_tier;
+
+/* Pinned host memory mapped into the device address space (the tier's host store). */
+int pf_host_alloc_mapped(int64_t bytes, void** host_ptr, void** dev_ptr);
+int pf_host_free(void* host_ptr);
+
+/* Make every tile the windows of specs_dev (planned: level/side/sx/sy) touch resident for
+ * batch id `batch` (>= 2, increasing per call): mark hits, claim victim slots no batch >=
+ * batch - 1 uses (clock hand), copy the missing tiles from the host store (zero-copy), update
+ * tile_map.  Stream-ordered, no host sync; the caller orders this call after the crops of
+ * batch - 2.  max_fill: the largest max_miss of the tiers; max_tiles_per_spec: tiles a window
+ * can touch (e.g. (ceil(side/T) + 1)^2).  A batch needing more tiles than a pool holds sets
+ * the slide's fault word to PF_ERR_CAPACITY (pf_slide_status). */
+int pf_tier_prefetch(const pf_slide_desc* slides_dev, const pf_tile_tier* tiers_dev, int32_t n_slides,
+                     const pf_patch_spec* specs_dev, int32_t n, int32_t batch, int32_t max_fill,
+                     int32_t max_tiles_per_spec, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Library                                                                   */
 /* ------------------------------------------------------------------------ */
 int pf_abi_version(void);

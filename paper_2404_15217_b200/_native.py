@@ -184,6 +184,9 @@ class _Lib:
             "pf_plan_regions": ([vp, vp, i32, vp], C.c_int),
             "pf_read_regions": ([vp, vp, i32, i32, i32, i32, vp, vp, vp, vp], C.c_int),
             "pf_read_region_fits": ([i32, i32, i32, C.POINTER(i32)], C.c_int),
+            "pf_host_alloc_mapped": ([i64, C.POINTER(vp), C.POINTER(vp)], C.c_int),
+            "pf_host_free": ([vp], C.c_int),
+            "pf_tier_prefetch": ([vp, vp, i32, vp, i32, i32, i32, i32, vp], C.c_int),
             "pf_slide_create": ([i32, i32, dbl, i32, i32, C.POINTER(vp)], C.c_int),
             "pf_slide_destroy": ([vp], C.c_int),
             "pf_slide_get_desc": ([vp, C.POINTER(SlideDesc)], C.c_int),

@@ -9,6 +9,23 @@
 
 #include "../../include/pf_b200.h"
 
+// PF_CHECKS builds (tools/build_variant.py checks ... -DPF_CHECKS; tests run against the result
+// with PF_B200_LIB) trap on any staged-buffer / table index outside its allocation: the
+// in-house substitute for compute-sanitizer, which this GPU pool does not allow.
+#ifdef PF_CHECKS
+#include <cstdio>
+#define PF_CHECK(cond)                                                                                   \
+    do {                                                                                                 \
+        if (!(cond)) {                                                                                   \
+            printf("PF_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,      \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                   \
+            __trap();                                                                                    \
+        }                                                                                                \
+    } while (0)
+#else
+#define PF_CHECK(cond) ((void)0)
+#endif
+
 namespace pf {
 
 // Thread-local last error; set by every failing entry point.
@@ -43,8 +60,8 @@ __device__ __forceinline__ const uint8_t* tile_ptr(const pf_slide_desc& s, int l
     const int32_t* map = reinterpret_cast<const int32_t*>(s.tile_map[level]);
     if (!map) return base + t * tile_bytes;
     const int32_t slot = __ldg(map + t);
-    if (slot == 0 && s.status_word)  // the zero hole: the read plan missed this tile (fail loudly)
-        *reinterpret_cast<volatile int32_t*>(s.status_word) = PF_ERR_OUT_OF_BOUNDS;
+    if (slot == 0 && s.status_word)  // the zero hole: the read plan missed this tile (fail loudly;
+        atomicCAS(reinterpret_cast<int*>(s.status_word), 0, PF_ERR_OUT_OF_BOUNDS);  // first fault sticks)
     return base + (size_t)slot * tile_bytes;
 }
 

@@ -263,7 +263,7 @@ __device__ inline int slow_attempt(const pf_sampler_config& cfg, const pf_sample
 // block.  The exact sequential path finishes whatever the table cannot decide.
 constexpr int kWalkThreads = 512;
 constexpr int kDrawCache = 256;
-constexpr int kFastDraws = 8192;  // slide draws precomputed per fast walk (int16 in shared memory)
+constexpr int kFastDraws = 8192;  // slide draws precomputed per fast walk (int32 in shared memory)
 
 __device__ inline double k_total_weight(const pf_sampler_config& cfg, const pf_sampler_slide* slides) {
     double total = 0.0;
@@ -343,7 +343,9 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
         // fast walk: every slide draw of the call precomputed in parallel (no rejected draw among
         // them), then one thread runs the chain a -> next_accept(slide_j, a) + 1 whose only
         // dependent load per draw is the next-accept table; bookkeeping is off the chain
-        int16_t* fdraw = reinterpret_cast<int16_t*>(na + (size_t)cfg.n_slides * window);
+        // int32 entries: 16-bit ones get packed in pairs by the compiler, which then waits on the
+        // prefetch load immediately
+        int32_t* fdraw = reinterpret_cast<int32_t*>(na + (((size_t)cfg.n_slides * window + 1) & ~(size_t)1));
         __shared__ int s_fast;
         int n_fd = 0;
         if (next_table) {
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                     }
                 }
                 if (sidx < 0) s_fast = 0;  // a rejected draw (p ~ n / 2^64): the general walk handles it
-                fdraw[i] = (int16_t)sidx;
+                fdraw[i] = sidx;
             }
             __syncthreads();
         }
@@ -390,7 +392,8 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                     s = fdraw[0];
                     j = 1;
                 }
-                int s_nxt = j < n_fd ? fdraw[j] : 0;
+                // two draws loaded ahead: a draw's load has landed long before the chain needs it
+                int s_nxt = fdraw[min(j, max(n_fd - 1, 0))], s_nxt2 = fdraw[min(j + 1, max(n_fd - 1, 0))];
                 const uint16_t* row = na + (size_t)max(s, 0) * window;
                 while (s >= 0 && emitted < n && status == PF_OK) {
                     const int budget = max_att - used;
@@ -398,8 +401,10 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                         mid_draw = true;
                         break;
                     }
+                    PF_CHECK(s >= 0 && s < cfg.n_slides && a >= 0 && a < window);
                     const int f = row[a];
                     if (f < min(a + budget, wlim)) {  // accepted: one spec, the draw is done
+                        PF_CHECK(emitted - s_first < window);
                         emit_list[emitted - s_first] = make_int2(s, f);
                         ++emitted;
                         a = f + 1;
@@ -423,7 +428,8 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                     s = s_nxt;
                     row = na + (size_t)s * window;
                     ++j;
-                    s_nxt = fdraw[min(j, n_fd - 1)];
+                    s_nxt = s_nxt2;
+                    s_nxt2 = fdraw[min(j + 1, n_fd - 1)];
                 }
                 if (!mid_draw) used = 0;
                 w.c_slide += (uint64_t)j;
@@ -671,7 +677,7 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     const int bm_in_smem = rounds > 0 && bm_bytes_all <= 160 * 1024;
     // next-accepted-offset table beside the bitmaps (uint16 offsets: window < 0xffff)
     const size_t nt_bytes = bm_bytes_all + ((size_t)cfg->n_slides * (window / 32) + 1) / 2 * 4 +
-                            (size_t)cfg->n_slides * window * 2 + (size_t)kFastDraws * 2;
+                            ((size_t)cfg->n_slides * window + 1) / 2 * 4 + (size_t)kFastDraws * 4;
     const int next_table = bm_in_smem && window < 0xffff && nt_bytes <= 200 * 1024;
     const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid),
                                       next_table ? nt_bytes : (bm_in_smem ? bm_bytes_all : (size_t)0));

@@ -166,20 +166,24 @@ __device__ int stage_level_rows(const pf_slide_desc& sd, int L, int X0, int Y0, 
     const int T = sd.tile_size;
     const int LW = sd.width[L], LH = sd.height[L];
     if (fast) {
-        const int tx0 = X0 / T, ntx = (X0 + w - 1) / T - tx0 + 1;
+        // only the 16-byte aligned span of each window row: [a0, a0 + 16 * nch) of the level row,
+        // chunk by chunk from whichever tile holds it (a tile row is 3T bytes, a multiple of 16)
+        const int a0 = (X0 * 3) & ~15;
+        const int nch = (X0 * 3 + w * 3 - a0 + 15) / 16;
         const int cpr = T * 3 / 16;
+        const int c0 = a0 / 16;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int rr = warp; rr < nr; rr += blockDim.x / 32) {
             const int Y = Y0 + rr;
             const int ty = Y / T, v = Y - ty * T;
             uint8_t* srow = stg + rr * row_bytes;
-            for (int t = 0; t < ntx; ++t) {
-                const uint8_t* grow = tile_ptr(sd, L, tx0 + t, ty) + (size_t)v * T * 3;
-                for (int ch = lane; ch < cpr; ch += 32) rr_cp_async16(srow + t * T * 3 + ch * 16, grow + ch * 16);
+            for (int ch = lane; ch < nch; ch += 32) {
+                const int c = c0 + ch, tx = c / cpr, e = c - tx * cpr;
+                rr_cp_async16(srow + ch * 16, tile_ptr(sd, L, tx, ty) + (size_t)v * T * 3 + e * 16);
             }
         }
         rr_cp_async_wait_all();
-        return (X0 - tx0 * T) * 3;
+        return X0 * 3 - a0;
     }
     for (int q = threadIdx.x; q < nr * w; q += blockDim.x) {
         const int rr = q / w, xx = q - rr * w;
@@ -250,6 +254,168 @@ struct RROut<PF_BF16> {
     using T = __nv_bfloat16;
 };
 
+// ---------------------------------------------------------------------------
+// Exact 2:1 PIL BILINEAR (side == 2 * out, window inside the level): BASELINE config 3's
+// 448 -> 224 reads.  Every interior output's taps are PIL's own 22-bit weights
+// (0.125, 0.375, 0.375, 0.125) * 2^22 = 2^19 * (1, 3, 3, 1), so
+//   (2^21 + sum w_k p_k) >> 22 == (p0 + 3 (p1 + p2) + p3 + 4) >> 3      (never clips),
+// computed on 16-bit lanes of packed words; the first and last output of each axis (3 clipped
+// taps, renormalised) take the table weights.  Bit-exact with the general path / Pillow.
+// Grid: (spec, band of kR2Rows output rows); specs it does not take exit at once.
+// ---------------------------------------------------------------------------
+constexpr int kR2Rows = 16;
+constexpr int kR2Threads = 256;
+
+__device__ __forceinline__ bool is_2x(const pf_patch_spec& sp, const pf_slide_desc& sd, int S) {
+    const int L = sp.level;
+    return sp.side == 2 * S && S >= 8 && (S % 4) == 0 && sp.sx >= 0 && sp.sy >= 0 && sp.sx + sp.side <= sd.width[L] &&
+           sp.sy + sp.side <= sd.height[L] && (sd.tile_size % 16) == 0;
+}
+
+// generic 3-tap PIL output of an axis edge: weights w[0..2] (22-bit), bytes p0..p2
+__device__ __forceinline__ uint32_t pil3(const int32_t* w, uint32_t p0, uint32_t p1, uint32_t p2) {
+    const int32_t a = (1 << 21) + (int32_t)p0 * w[0] + (int32_t)p1 * w[1] + (int32_t)p2 * w[2];
+    return clip_shift(a, 22);
+}
+
+template <int kDtype, int kS>
+__global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_desc* slides, const pf_patch_spec* specs,
+                                                                int S_rt, int layout, int n_bands, NormParams np,
+                                                                void* out_v) {
+    using OT = typename RROut<kDtype>::T;
+    const int S = kS ? kS : S_rt;  // compile-time for the BASELINE size: index math without divisions
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int spec_i = blockIdx.x / n_bands, band = blockIdx.x - spec_i * n_bands;
+    const pf_patch_spec sp = specs[spec_i];
+    const pf_slide_desc& sd = slides[sp.slide];
+    if (!is_2x(sp, sd, S)) return;
+    const int Y0 = band * kR2Rows, Y1 = min(S, Y0 + kR2Rows);
+    if (Y0 >= S) return;
+    const int lay = layout & 0xff;
+    const int L = sp.level, T = sd.tile_size;
+    const int side = 2 * S;
+    // edge weights (first / last output of an axis), PIL's own computation
+    __shared__ int32_t s_w0[3], s_wl[3];
+    if (threadIdx.x < 2) {
+        const AxisPlan ap = axis_plan(side, S);
+        double w[8];
+        int xmin;
+        const int xs = axis_weights(ap, side, threadIdx.x == 0 ? 0 : S - 1, &xmin, w);
+        for (int k = 0; k < 3; ++k) (threadIdx.x == 0 ? s_w0 : s_wl)[k] = k < xs ? quantise_weight(w[k], 22) : 0;
+    }
+    OT* lut = reinterpret_cast<OT*>(smem);
+    uint8_t* stg = smem + ((3 * 256 * sizeof(OT) + 15) & ~size_t(15));
+    if constexpr (kDtype != PF_U8)
+        for (int i = threadIdx.x; i < 3 * 256; i += kR2Threads) {
+            const int c = i >> 8;
+            const float f = __fdiv_rn(__fdiv_rn((float)(i & 255), 255.0f) - np.mean[c], np.stdv[c]);
+            if constexpr (kDtype == PF_F32) lut[i] = f;
+            else lut[i] = __float2bfloat16_rn(f);
+        }
+    // source rows of the band: output y uses rows 2y - 1 .. 2y + 2 (y = 0: 0..2; y = S-1: 2S-3..2S-1)
+    const int R0 = max(0, 2 * Y0 - 1), R1 = min(side, 2 * (Y1 - 1) + 3);
+    const int nr = R1 - R0;
+    const int a0 = (sp.sx * 3) & ~15, off = sp.sx * 3 - a0;
+    const int nch = (off + side * 3 + 15) / 16;
+    const int pitch = nch * 16 + 16;
+    uint8_t* hb = stg + (size_t)nr * pitch;  // [3][nr][S] horizontal-pass output
+    PF_CHECK(nr <= 2 * kR2Rows + 2 && (int)((3 * 256 * sizeof(OT) + 15) & ~size_t(15)) + nr * pitch + 3 * nr * S <=
+             (int)(3 * 256 * 4 + (2 * kR2Rows + 2) * ((15 + 6 * S + 15) / 16 * 16 + 16) + 3 * (2 * kR2Rows + 2) * S + 64));
+    const int cpr = T * 3 / 16, c0 = a0 / 16;
+    const int tx0 = c0 / cpr, e0 = c0 - tx0 * cpr;
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int rr = warp; rr < nr; rr += kR2Threads / 32) {
+            const int Y = sp.sy + R0 + rr;
+            const int ty = Y / T, v = Y - ty * T;
+            for (int ch = lane; ch < nch; ch += 32) {
+                int e = e0 + ch, tx = tx0;
+                while (e >= cpr) e -= cpr, ++tx;  // a window row spans at most a few tiles
+                rr_cp_async16(stg + rr * pitch + ch * 16, tile_ptr(sd, L, tx, ty) + (size_t)v * T * 3 + e * 16);
+            }
+        }
+        rr_cp_async_wait_all();
+    }
+    __syncthreads();
+    // horizontal pass: item = (staged row, output column)
+    for (int q = threadIdx.x; q < nr * S; q += kR2Threads) {
+        const int rr = q / S, x = q - rr * S;
+        const uint8_t* row = stg + rr * pitch + off;
+        uint8_t* d = hb + rr * S + x;
+        if (x == 0 || x == S - 1) {
+            const uint8_t* p = row + (x == 0 ? 0 : (side - 3) * 3);
+            const int32_t* w = x == 0 ? s_w0 : s_wl;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) d[c * nr * S] = (uint8_t)pil3(w, p[c], p[3 + c], p[6 + c]);
+            continue;
+        }
+        const int b0 = off + (2 * x - 1) * 3;  // 12 bytes: pixels 2x-1 .. 2x+2
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(stg + rr * pitch + (b0 & ~3));
+        const uint32_t sh = (uint32_t)(b0 & 3) * 8;
+        const uint32_t r0 = wp[0], r1 = wp[1], r2 = wp[2], r3 = wp[3];
+        const uint32_t A0 = __funnelshift_r(r0, r1, sh), A1 = __funnelshift_r(r1, r2, sh), A2 = __funnelshift_r(r2, r3, sh);
+        // bytes: A0 = R0 G0 B0 R1, A1 = G1 B1 R2 G2, A2 = B2 R3 G3 B3
+        const uint32_t p0[3] = {A0 & 0xffu, (A0 >> 8) & 0xffu, (A0 >> 16) & 0xffu};
+        const uint32_t p1[3] = {A0 >> 24, A1 & 0xffu, (A1 >> 8) & 0xffu};
+        const uint32_t p2[3] = {(A1 >> 16) & 0xffu, A1 >> 24, A2 & 0xffu};
+        const uint32_t p3[3] = {(A2 >> 8) & 0xffu, (A2 >> 16) & 0xffu, A2 >> 24};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) d[c * nr * S] = (uint8_t)((p0[c] + p3[c] + 3u * (p1[c] + p2[c]) + 4u) >> 3);
+    }
+    __syncthreads();
+    // vertical pass: item = (output row, 4 columns); 16-bit lanes of packed words
+    const size_t plane = (size_t)S * S;
+    OT* o = reinterpret_cast<OT*>(out_v) + (size_t)spec_i * 3 * plane;
+    const int G = S / 4;
+    for (int q = threadIdx.x; q < (Y1 - Y0) * G; q += kR2Threads) {
+        const int yy = q / G, x0 = (q - yy * G) * 4;
+        const int y = Y0 + yy;
+        uint32_t px[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const uint8_t* col = hb + (size_t)c * nr * S + x0;
+            if (y == 0 || y == S - 1) {
+                const int rb = (y == 0 ? 0 : side - 3) - R0;
+                const int32_t* w = y == 0 ? s_w0 : s_wl;
+                uint32_t v = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    v |= pil3(w, col[(rb) * S + k], col[(rb + 1) * S + k], col[(rb + 2) * S + k]) << (8 * k);
+                px[c] = v;
+            } else {
+                const int rb = 2 * y - 1 - R0;
+                const uint32_t w0 = *reinterpret_cast<const uint32_t*>(col + rb * S);
+                const uint32_t w1 = *reinterpret_cast<const uint32_t*>(col + (rb + 1) * S);
+                const uint32_t w2 = *reinterpret_cast<const uint32_t*>(col + (rb + 2) * S);
+                const uint32_t w3 = *reinterpret_cast<const uint32_t*>(col + (rb + 3) * S);
+                const uint32_t m = 0x00ff00ffu;
+                const uint32_t lo = ((w0 & m) + (w3 & m) + 3u * ((w1 & m) + (w2 & m)) + 0x00040004u) >> 3;
+                const uint32_t hi = (((w0 >> 8) & m) + ((w3 >> 8) & m) + 3u * (((w1 >> 8) & m) + ((w2 >> 8) & m)) +
+                                     0x00040004u) >> 3;
+                px[c] = (lo & m) | ((hi & m) << 8);
+            }
+        }
+        if (kDtype == PF_U8 && lay == PF_HWC) {  // 4 pixels x RGB = 12 bytes = 3 words (offset a multiple of 12)
+            const uint32_t R = px[0], Gc = px[1], B = px[2];
+            uint32_t* dst = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(o) + ((size_t)y * S + x0) * 3);
+            // r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3
+            dst[0] = __byte_perm(__byte_perm(R, Gc, 0x1040u), B, 0x3410u);
+            dst[1] = __byte_perm(__byte_perm(Gc, B, 0x2051u), R, 0x3610u);
+            dst[2] = __byte_perm(__byte_perm(B, R, 0x3072u), Gc, 0x3710u);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const uint8_t v = (uint8_t)(px[c] >> (8 * k));
+                    const size_t idx = lay == PF_HWC ? ((size_t)y * S + x0 + k) * 3 + c : c * plane + (size_t)y * S + x0 + k;
+                    if constexpr (kDtype == PF_U8) reinterpret_cast<uint8_t*>(o)[idx] = v;
+                    else o[idx] = lut[c * 256 + v];
+                }
+        }
+    }
+}
+
 template <int kDtype>
 __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide_desc* slides,
                                                                   const pf_patch_spec* specs, int S, int layout,
@@ -267,6 +433,7 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
     const bool pass = side == S;
     if (pass && skip_pass) return;
     if (band * kRRBand >= S) return;
+    if (!pass && is_2x(sp, sd, S)) return;  // resample2x_kernel takes it
     OT* out = reinterpret_cast<OT*>(out_v);
     // LUT for the epilogue
     OT* lut = reinterpret_cast<OT*>(smem);
@@ -292,7 +459,7 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
         const int nr = y1 - y0;
         const int X0 = sp.sx, Y0 = sp.sy + y0;
         const bool fast = X0 >= 0 && Y0 >= 0 && X0 + S <= LW && Y0 + nr <= LH && (T % 16) == 0;
-        const int row_bytes = fast ? ((X0 + S - 1) / T - X0 / T + 1) * T * 3 : ((S * 3 + 15) & ~15);
+        const int row_bytes = fast ? (((X0 * 3) & 15) + S * 3 + 15) & ~15 : ((S * 3 + 15) & ~15);
         const int base = stage_level_rows(sd, L, X0, Y0, S, nr, work, row_bytes, fast);
         __syncthreads();
         if (lay == PF_NCHW && (S % 4) == 0) {
@@ -348,6 +515,7 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
     const int nch = (off + side * 3 + 15) / 16;
     const int pitch = nch * 16 + 16;
     const int cap = (buf_bytes - 3 * S * 4) / (2 * pitch + 3 * S);  // source rows per band
+    PF_CHECK(cap >= 4);  // pf_read_region_fits keeps such windows off this kernel
     if (cap < 4) return;  // host checks the window fits (out_size <= 512)
     uint8_t* hb = buf + 2 * cap * pitch;  // [3][cap + 4][S]
     const int hplane = (cap + 4) * S;
@@ -628,13 +796,36 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
     const long long grid = (long long)n * n_bands;
     cudaStream_t st = as_stream(stream);
     int rc;
+    // the exact 2:1 kernel's shared memory: LUT + (2 * kR2Rows + 2) staged rows + planar H output
+    const int r2_rows = 2 * kR2Rows + 2;
+    const int r2_smem = 3 * 256 * 4 + r2_rows * ((15 + 6 * out_size + 15) / 16 * 16 + 16) + 3 * r2_rows * out_size + 64;
+    const int r2_bands = (out_size + kR2Rows - 1) / kR2Rows;
+    const bool r2 = r2_smem <= 160 * 1024;
 #define PF_RR_LAUNCH(DT)                                                                                          \
     rc = check_cuda(cudaFuncSetAttribute(read_regions_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                                          kRRSmem),                                                                \
                     "cudaFuncSetAttribute");                                                                      \
     if (rc) return rc;                                                                                            \
     read_regions_kernel<DT><<<(unsigned)grid, kRRThreads, kRRSmem, st>>>(slides_dev, specs_dev, out_size, layout,  \
-                                                                          n_bands, np, out);
+                                                                          n_bands, np, out);                      \
+    if (r2) {                                                                                                     \
+        if ((rc = after_launch("read_regions_kernel"))) return rc;                                                \
+        if (out_size == 224) {                                                                                    \
+            rc = check_cuda(cudaFuncSetAttribute(resample2x_kernel<DT, 224>,                                      \
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, r2_smem),           \
+                            "cudaFuncSetAttribute");                                                              \
+            if (rc) return rc;                                                                                    \
+            resample2x_kernel<DT, 224><<<(unsigned)((long long)n * r2_bands), kR2Threads, r2_smem, st>>>(         \
+                slides_dev, specs_dev, out_size, layout, r2_bands, np, out);                                      \
+        } else {                                                                                                  \
+            rc = check_cuda(cudaFuncSetAttribute(resample2x_kernel<DT, 0>,                                        \
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, r2_smem),           \
+                            "cudaFuncSetAttribute");                                                              \
+            if (rc) return rc;                                                                                    \
+            resample2x_kernel<DT, 0><<<(unsigned)((long long)n * r2_bands), kR2Threads, r2_smem, st>>>(           \
+                slides_dev, specs_dev, out_size, layout, r2_bands, np, out);                                      \
+        }                                                                                                         \
+    }
     switch (dtype) {
         case PF_U8: PF_RR_LAUNCH(PF_U8) break;
         case PF_F32: PF_RR_LAUNCH(PF_F32) break;

@@ -200,9 +200,17 @@ class MultiCropLoader:
                                       dtype=tdt, device="cuda")
         self.out_local = torch.empty((self.mc.n_local, batch_size, 3, self.mc.local_size, self.mc.local_size),
                                      dtype=tdt, device="cuda")
+        # host-backed tile tiers (tier.py): each sampled batch's tiles are made resident on the
+        # sampler's stream right after sampling, a batch ahead of its crops
+        from .tier import TierSet
+
+        ts = TierSet(self.slide_set)
+        self.tiers = ts if ts.active else None
 
     def _sample(self, slot: int, st) -> None:
         self.specs_from.next_batch(self.batch_size, out=self.specs_slots[slot], stream=st)
+        if self.tiers is not None:
+            self.tiers.prefetch(self.specs_slots[slot], self.batch_size, stream=st)
 
     def next_batch(self, stream=None, marks: list | None = None) -> dict:
         """Enqueue one step and return its device tensors.
@@ -250,6 +258,10 @@ class MultiCropLoader:
         if self.prefetch:
             nxt = 1 - cur
             self._side.wait_event(self._free[nxt])  # step k-1 finished reading that slot
+            if self.needs_resample:  # the next sampler overlaps the multi-crop, not the resample
+                done = torch.cuda.Event()
+                done.record(st)
+                self._side.wait_event(done)
             self._sample(nxt, self._side)
             self._ready[nxt] = torch.cuda.Event()
             self._ready[nxt].record(self._side)

@@ -181,7 +181,7 @@ class GpuSlide:
         self.desc = self._make_desc()
         self._sets = weakref.WeakSet()  # SlideSets holding a device copy of self.desc
 
-    def compact(self, plan) -> None:
+    def compact(self, plan, levels=None) -> None:
         """Keep only the planned tiles resident (residency.reachable_tiles): each level becomes
         [1 + n_resident] tile slots (slot 0 = zero hole) plus an int32 slot map; the dense level is
         freed.  Reads of non-resident tiles return zeros (pf_slide_desc.tile_map)."""
@@ -190,6 +190,8 @@ class GpuSlide:
         # in-flight reads (any stream) of the dense levels finish before they are freed
         torch.cuda.synchronize()
         for li, keep in enumerate(plan):
+            if levels is not None and li not in levels:
+                continue
             if self.tile_maps[li] is not None:
                 raise ValueError(f"level {li} is already compacted")
             nx, ny = self.record.tile_grid(li)
@@ -392,6 +394,14 @@ class GpuSlide:
         self.require_resident(specs[0])
         if getattr(self, "_own_set", None) is None:
             self._own_set = SlideSet([self])
+        if getattr(self, "tier", None) is not None:  # host-backed level: bring the window's tiles in
+            from .tier import TierSet
+
+            if getattr(self, "_own_tiers", None) is None:
+                self._own_tiers = TierSet(self._own_set)
+            import torch
+
+            self._own_tiers.prefetch(torch.from_numpy(specs.view(np.uint8).reshape(1, 64)).cuda(), 1)
         out = self._own_set.read_regions(specs, out_size)
         if self.compacted:
             self.check_status()

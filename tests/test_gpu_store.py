@@ -153,3 +153,29 @@ def test_ingest_image_writes_the_reference_store(cuda, golden_arrays, goldens, t
         back = pf.GpuSlide.from_store(tmp_path, "s0")
         for li in range(len(rec.levels)):
             assert cuda.equal(back.level_array(li), slide.level_array(li))
+
+
+def test_resample_2x_fast_path_exact(pf, cuda):
+    """side == 2 * out windows take resample2x_kernel (PIL's 2:1 weights as exact integer taps):
+    byte-identical with the oracle's PIL resize for every layout and dtype, including the
+    first/last output rows and columns (clipped, renormalised taps) and out sizes that are not
+    multiples of 4 (general kernel)."""
+    rs = np.random.default_rng(21)
+    img = rs.integers(0, 256, size=(900, 1100, 3), dtype=np.uint8)
+    s = pf.GpuSlide.from_array(img, "r2", 0.25, tile_size=128, downsample_factor=4)
+    ss = pf.SlideSet([s])
+    levels = port.pyramid(img, 128, 4)
+    mpps = [lv.mpp for lv in s.record.levels]
+    dss = [lv.downsample for lv in s.record.levels]
+    for out in (8, 12, 32, 60, 96, 224, 30):
+        reqs = []
+        for _ in range(6):
+            fp = 2 * out
+            x, y = int(rs.integers(0, 1100 - fp)), int(rs.integers(0, 900 - fp))
+            reqs.append((0, (x, y, fp, fp), 0.5, out))
+        specs = pf.store.plan_specs(reqs, ss.records)
+        assert all(int(sp["side"]) == 2 * out for sp in specs)
+        want = np.stack([port.read_region(levels, mpps, dss, r[1], 0.5, out) for r in reqs])
+        assert np.array_equal(ss.read_regions(specs, out).cpu().numpy(), want), out
+        f32 = ss.read_regions(specs, out, dtype="f32", layout="nchw").cpu().numpy()
+        assert np.array_equal(f32, port.normalize_patch(want).transpose(0, 3, 1, 2)), out
