@@ -159,8 +159,8 @@ def test_full_size_read_regions_mixed_mpp(pf, c2):
     f32 = ss.read_regions(specs, 224, dtype="f32", mean=mean, std=std).cpu().numpy()
     hs = smp.to_patch_specs(specs)
     slides = {s.record.slide_id: s for s, _ in c2}
-    picked = [i for i in range(256) if hs[i].target_mpp == 0.25][:4] + [i for i in range(256) if hs[i].target_mpp == 0.5][:4]
-    assert len(picked) == 8
+    picked = [i for i in range(256) if hs[i].target_mpp == 0.25][:32] + [i for i in range(256) if hs[i].target_mpp == 0.5][:32]
+    assert len(picked) == 64
     for i in picked:
         sp = hs[i]
         s = slides[sp.slide_id]
@@ -171,6 +171,39 @@ def test_full_size_read_regions_mixed_mpp(pf, c2):
                                 sp.target_mpp, 224)
         assert np.array_equal(u8[i], want), (i, sp)
         assert np.array_equal(f32[i], port.normalize_patch(want, mean, std))
+
+
+def test_full_size_mixed_mpp_multicrop_vs_torchvision(pf, c2):
+    """C3 at full size: 0.5-mpp specs are PIL-resampled 448 -> 224 (resample2x_kernel) and cut by
+    the multi-crop from that buffer; both stages against their oracles for 48 patches."""
+    torch = pytest.importorskip("torch")
+    ss = pf.SlideSet([s for s, _ in c2])
+    cfg = pf.SamplerConfig(patch_size=224, min_foreground=0.40, target_mpps=[(0.25, 1.0), (0.5, 1.0)], seed=SEED + 1)
+    smp = pf.GpuSampler(cfg, c2, slide_set=ss)
+    specs = smp.next_batch(256)
+    mc = pf.mc.MultiCropConfig()
+    params = pf.mc.crop_params(mc, 256, seed=11, step=2)
+    src = ss.read_regions(specs, 224, planned=True)
+    g, l = pf.mc.multicrop(ss, specs, params, mc, dtype="u8", src_hwc=src)
+    torch.cuda.synchronize()
+    hs, prm = smp.to_patch_specs(specs), pf.mc.params_host(params)
+    g, l, srcs = g.cpu().numpy(), l.cpu().numpy(), src.cpu().numpy()
+    slides = {s.record.slide_id: s for s, _ in c2}
+    picked = [i for i in range(256) if hs[i].target_mpp == 0.5][:24] + [i for i in range(256) if hs[i].target_mpp == 0.25][:24]
+    for i in picked:
+        sp = hs[i]
+        s = slides[sp.slide_id]
+        x0, y0 = max(0, sp.x - 2), max(0, sp.y - 2)
+        crop = _region(s, 0, x0, y0, min(W, sp.x + sp.width + 2) - x0, min(H, sp.y + sp.height + 2) - y0)
+        mpps = [lv.mpp for lv in s.record.levels]
+        want_src = port.read_region([crop], mpps, [1.0] * len(mpps), (sp.x - x0, sp.y - y0, sp.width, sp.height),
+                                    sp.target_mpp, 224)
+        if sp.target_mpp == 0.5:
+            assert np.array_equal(srcs[i], want_src), i
+        for c in range(mc.n_crops):
+            want = A.torchvision_crop(want_src, prm[i, c])
+            got = (g[c, i] if c < mc.n_global else l[c - mc.n_global, i]).transpose(1, 2, 0)
+            assert np.abs(got.astype(int) - want.astype(int)).max() <= 1, (i, c)
 
 
 @pytest.fixture(scope="module")
@@ -193,7 +226,7 @@ def test_full_batch_sampled_patches_vs_torchvision(pf, c2, batch):
     slides = {s.record.slide_id: s for s, _ in c2}
     g, l = g.cpu().numpy(), l.cpu().numpy()
     diff, total = 0, 0
-    for i in np.random.default_rng(1).choice(1024, 6, replace=False):
+    for i in np.random.default_rng(1).choice(1024, 128, replace=False):  # 1280 crops vs torchvision
         sp = hs[i]
         src = _region(slides[sp.slide_id], 0, sp.x, sp.y, 224, 224)  # C2: 0.25 mpp = level 0, no resample
         for c in range(cfg.n_crops):
