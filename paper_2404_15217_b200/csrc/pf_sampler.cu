@@ -323,20 +323,29 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                 }
             }
             __syncthreads();
+            // entry (slide, a) = where a fresh draw starting at offset a leaves the walk:
+            //   f + 1            its first accepted attempt f (a spec),
+            //   0x8000 | a + M   no accept within M = max_attempts (ExhaustedAttemptsError),
+            //   0xffff           the window (or a rejected coords draw) ends inside the draw
+            const int wlim_t = min(window, *ws.reject_at);
             for (int sl = 0; sl < cfg.n_slides; ++sl)
             for (int a = tid; a < window; a += kWalkThreads) {
                 const int i = sl * window + a;
                 const uint32_t* bm = bm_all + (size_t)sl * words;
                 const int wd = a >> 5;
                 const uint32_t m = bm[wd] & (0xffffffffu << (a & 31));
-                int f = 0xffff;
+                int f = 0x7fffffff;
                 if (m) {
                     f = wd * 32 + __ffs(m) - 1;
                 } else if (wd + 1 < words) {
                     const int w2 = nextw[sl * words + wd + 1];
                     if (w2 < words) f = w2 * 32 + __ffs(bm[w2]) - 1;
                 }
-                na[i] = (uint16_t)f;
+                uint32_t e;
+                if (f < min(a + max_att, wlim_t)) e = (uint32_t)(f + 1);
+                else if (a + max_att <= wlim_t) e = 0x8000u | (uint32_t)(a + max_att);
+                else e = 0xffffu;
+                na[i] = (uint16_t)e;
             }
             __syncthreads();
         }
@@ -383,53 +392,65 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                 int64_t failures = w.failures;
                 int status = w.status;
                 bool mid_draw = false;
-                // the draw in hand (s, its table row, attempts it already used) and the next one,
-                // loaded ahead so the chain per draw is one table load + compare
                 int s = w.cur_slide;
-                if (s >= 0) {
+                if (s >= 0) {  // a draw resumed from the previous call: its budget is max_att - cur_used
                     used = w.cur_used;
-                } else if (n_fd > 0) {
-                    s = fdraw[0];
-                    j = 1;
-                }
-                // two draws loaded ahead: a draw's load has landed long before the chain needs it
-                int s_nxt = fdraw[min(j, max(n_fd - 1, 0))], s_nxt2 = fdraw[min(j + 1, max(n_fd - 1, 0))];
-                const uint16_t* row = na + (size_t)max(s, 0) * window;
-                while (s >= 0 && emitted < n && status == PF_OK) {
                     const int budget = max_att - used;
-                    if (a >= wlim) {  // the window ends at this draw's first attempt
-                        mid_draw = true;
-                        break;
-                    }
-                    PF_CHECK(s >= 0 && s < cfg.n_slides && a >= 0 && a < window);
-                    const int f = row[a];
-                    if (f < min(a + budget, wlim)) {  // accepted: one spec, the draw is done
-                        PF_CHECK(emitted - s_first < window);
+                    const int span = min(budget, wlim);
+                    const uint32_t* bm = bm_all + (size_t)s * words;
+                    int f = 0x7fffffff;
+                    for (int x = 0; x < span && f == 0x7fffffff; ++x)
+                        if ((bm[x >> 5] >> (x & 31)) & 1u) f = x;
+                    if (f != 0x7fffffff) {
                         emit_list[emitted - s_first] = make_int2(s, f);
                         ++emitted;
                         a = f + 1;
                         failures = 0;
-                    } else if (a + budget <= wlim) {  // ExhaustedAttemptsError: redraw, no seq consumed
-                        a += budget;
-                        if (++failures >= flimit) status = PF_ERR_NO_SAMPLABLE;
-                    } else {  // the window (or a rejected coords draw) ends inside this draw
-                        used += wlim - a;
-                        a = wlim;
-                        mid_draw = true;
-                        break;
-                    }
-                    // next draw (only if the stream continues: no draw is taken past the n-th spec
-                    // or a NoSamplableSlideError)
-                    used = 0;
-                    if (emitted >= n || status != PF_OK || j == n_fd) {  // j == n_fd: the next round continues
                         s = -1;
-                        break;
+                    } else if (span == budget) {
+                        a = budget;
+                        if (++failures >= flimit) status = PF_ERR_NO_SAMPLABLE;
+                        s = -1;
+                    } else {
+                        a = span;
+                        used += span;
+                        mid_draw = true;
                     }
-                    s = s_nxt;
-                    row = na + (size_t)s * window;
-                    ++j;
-                    s_nxt = s_nxt2;
-                    s_nxt2 = fdraw[min(j + 1, n_fd - 1)];
+                }
+                // the chain: one table load per draw, a = entry (the common case needs no ALU op);
+                // the next draw's slide and table row are known ahead
+                if (!mid_draw && emitted < n && status == PF_OK && n_fd > 0) {
+                    int sj = fdraw[0];
+                    int s_nxt = fdraw[min(1, n_fd - 1)];
+                    const uint16_t* row = na + (size_t)sj * window;
+                    j = 1;
+                    while (true) {
+                        if (a >= wlim) {  // the window ends at this draw's first attempt
+                            s = sj, used = 0, mid_draw = true;
+                            break;
+                        }
+                        const uint32_t e = row[a];
+                        if (e < 0x8000u) {  // accepted at e - 1
+                            PF_CHECK(emitted - s_first < window);
+                            emit_list[emitted - s_first] = make_int2(sj, (int)e - 1);
+                            ++emitted;
+                            a = (int)e;
+                            failures = 0;
+                        } else if (e != 0xffffu) {  // exhausted
+                            a = (int)(e & 0x7fffu);
+                            if (++failures >= flimit) status = PF_ERR_NO_SAMPLABLE;
+                        } else {  // the window ends inside this draw
+                            used = wlim - a;
+                            a = wlim;
+                            s = sj, mid_draw = true;
+                            break;
+                        }
+                        if (emitted >= n || status != PF_OK || j == n_fd) break;  // j == n_fd: next round
+                        sj = s_nxt;
+                        row = na + (size_t)sj * window;
+                        ++j;
+                        s_nxt = fdraw[min(j, n_fd - 1)];
+                    }
                 }
                 if (!mid_draw) used = 0;
                 w.c_slide += (uint64_t)j;
@@ -494,10 +515,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                 const int budget = max_att - w.cur_used;
                 const int span = min(budget, wlim - a0);
                 int found = -1;
-                if (span > 0 && next_table) {
-                    const int f = na[w.cur_slide * window + a0];
-                    if (f < a0 + span) found = f;
-                } else if (span > 0) {
+                if (span > 0) {
                     const uint32_t* bm = bm_all + (size_t)w.cur_slide * words;
                     const int wfirst = a0 >> 5, wlast = (a0 + span - 1) >> 5;
                     // common case first (acceptance ~0.5): the next accepted offset lies in a0's word
@@ -678,7 +696,7 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     // next-accepted-offset table beside the bitmaps (uint16 offsets: window < 0xffff)
     const size_t nt_bytes = bm_bytes_all + ((size_t)cfg->n_slides * (window / 32) + 1) / 2 * 4 +
                             ((size_t)cfg->n_slides * window + 1) / 2 * 4 + (size_t)kFastDraws * 4;
-    const int next_table = bm_in_smem && window < 0xffff && nt_bytes <= 200 * 1024;
+    const int next_table = bm_in_smem && window + cfg->max_attempts < 0x7fff && nt_bytes <= 200 * 1024;
     const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid),
                                       next_table ? nt_bytes : (bm_in_smem ? bm_bytes_all : (size_t)0));
     rc = check_cuda(cudaFuncSetAttribute(sample_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)walk_smem),

@@ -263,7 +263,7 @@ struct RROut<PF_BF16> {
 // taps, renormalised) take the table weights.  Bit-exact with the general path / Pillow.
 // Grid: (spec, band of kR2Rows output rows); specs it does not take exit at once.
 // ---------------------------------------------------------------------------
-constexpr int kR2Rows = 16;
+constexpr int kR2Rows = 8;
 constexpr int kR2Threads = 256;
 
 __device__ __forceinline__ bool is_2x(const pf_patch_spec& sp, const pf_slide_desc& sd, int S) {
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
     const int nr = R1 - R0;
     const int a0 = (sp.sx * 3) & ~15, off = sp.sx * 3 - a0;
     const int nch = (off + side * 3 + 15) / 16;
-    const int pitch = nch * 16 + 16;
+    const int pitch = nch * 16 + 16;  // the last group's 9-word load reads <= 12 bytes past the span
     uint8_t* hb = stg + (size_t)nr * pitch;  // [3][nr][S] horizontal-pass output
     PF_CHECK(nr <= 2 * kR2Rows + 2 && (int)((3 * 256 * sizeof(OT) + 15) & ~size_t(15)) + nr * pitch + 3 * nr * S <=
              (int)(3 * 256 * 4 + (2 * kR2Rows + 2) * ((15 + 6 * S + 15) / 16 * 16 + 16) + 3 * (2 * kR2Rows + 2) * S + 64));
@@ -337,30 +337,59 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
         rr_cp_async_wait_all();
     }
     __syncthreads();
-    // horizontal pass: item = (staged row, output column)
-    for (int q = threadIdx.x; q < nr * S; q += kR2Threads) {
-        const int rr = q / S, x = q - rr * S;
-        const uint8_t* row = stg + rr * pitch + off;
-        uint8_t* d = hb + rr * S + x;
-        if (x == 0 || x == S - 1) {
-            const uint8_t* p = row + (x == 0 ? 0 : (side - 3) * 3);
-            const int32_t* w = x == 0 ? s_w0 : s_wl;
+    // horizontal pass: item = (staged row, 4 output columns): source pixels 2x0-1 .. 2x0+8 as
+    // 32 bytes from 9 aligned words + funnel shifts, 4 outputs per channel packed into one word;
+    // the first and last group (clipped taps at x = 0 and x = S-1) per column
+    const int G4h = S / 4;
+    auto store3 = [&](int rr, int x0, const uint32_t (&w)[3]) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) d[c * nr * S] = (uint8_t)pil3(w, p[c], p[3 + c], p[6 + c]);
-            continue;
-        }
-        const int b0 = off + (2 * x - 1) * 3;  // 12 bytes: pixels 2x-1 .. 2x+2
+        for (int c = 0; c < 3; ++c) *reinterpret_cast<uint32_t*>(hb + (size_t)c * nr * S + rr * S + x0) = w[c];
+    };
+    // interior groups (x0 = 4 .. S-8): no per-column branches inside a warp
+    for (int q = threadIdx.x; q < nr * (G4h - 2); q += kR2Threads) {
+        const int rr = q / (G4h - 2), x0 = (q - rr * (G4h - 2) + 1) * 4;
+        const int b0 = off + (2 * x0 - 1) * 3;  // 30 bytes: pixels 2x0-1 .. 2x0+8
         const uint32_t* wp = reinterpret_cast<const uint32_t*>(stg + rr * pitch + (b0 & ~3));
         const uint32_t sh = (uint32_t)(b0 & 3) * 8;
-        const uint32_t r0 = wp[0], r1 = wp[1], r2 = wp[2], r3 = wp[3];
-        const uint32_t A0 = __funnelshift_r(r0, r1, sh), A1 = __funnelshift_r(r1, r2, sh), A2 = __funnelshift_r(r2, r3, sh);
-        // bytes: A0 = R0 G0 B0 R1, A1 = G1 B1 R2 G2, A2 = B2 R3 G3 B3
-        const uint32_t p0[3] = {A0 & 0xffu, (A0 >> 8) & 0xffu, (A0 >> 16) & 0xffu};
-        const uint32_t p1[3] = {A0 >> 24, A1 & 0xffu, (A1 >> 8) & 0xffu};
-        const uint32_t p2[3] = {(A1 >> 16) & 0xffu, A1 >> 24, A2 & 0xffu};
-        const uint32_t p3[3] = {(A2 >> 8) & 0xffu, (A2 >> 16) & 0xffu, A2 >> 24};
+        uint32_t r[9], A[8], outw[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) d[c * nr * S] = (uint8_t)((p0[c] + p3[c] + 3u * (p1[c] + p2[c]) + 4u) >> 3);
+        for (int i = 0; i < 9; ++i) r[i] = wp[i];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) A[i] = __funnelshift_r(r[i], r[i + 1], sh);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            uint32_t pb[10];  // channel c of the 10 pixels: byte 3i + c
+#pragma unroll
+            for (int i = 0; i < 10; ++i) pb[i] = (A[(3 * i + c) >> 2] >> (8 * ((3 * i + c) & 3))) & 0xffu;
+            uint32_t o = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                o |= ((pb[2 * k] + pb[2 * k + 3] + 3u * (pb[2 * k + 1] + pb[2 * k + 2]) + 4u) >> 3) << (8 * k);
+            outw[c] = o;
+        }
+        store3(rr, x0, outw);
+    }
+    // the first and last group of every row: the clipped edge taps at x = 0 and x = S-1
+    for (int q = threadIdx.x; q < 2 * nr; q += kR2Threads) {
+        const int rr = q >> 1, x0 = (q & 1) ? S - 4 : 0;
+        const uint8_t* row = stg + rr * pitch + off;
+        uint32_t o[3] = {0u, 0u, 0u};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int x = x0 + k;
+            if (x == 0 || x == S - 1) {
+                const uint8_t* p = row + (x == 0 ? 0 : (side - 3) * 3);
+                const int32_t* w = x == 0 ? s_w0 : s_wl;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) o[c] |= pil3(w, p[c], p[3 + c], p[6 + c]) << (8 * k);
+            } else {
+                const uint8_t* p = row + (2 * x - 1) * 3;
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    o[c] |= (((uint32_t)p[c] + p[9 + c] + 3u * ((uint32_t)p[3 + c] + p[6 + c]) + 4u) >> 3) << (8 * k);
+            }
+        }
+        store3(rr, x0, o);
     }
     __syncthreads();
     // vertical pass: item = (output row, 4 columns); 16-bit lanes of packed words

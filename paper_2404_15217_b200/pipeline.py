@@ -88,27 +88,39 @@ def run_loader(specs, slides, config: LoaderConfig | None = None, batch: int | N
         errors.append(LoaderFailure(spec, exc))
 
     def load_chunk(chunk):
-        """[(pixels or None, exception or None)] in chunk order."""
+        """[(pixels or None, exception or None)] in chunk order: one host plan of the chunk (the
+        reference's read_region checks per spec), one device read per out_size."""
         res: list = [(None, None)] * len(chunk)
-        good: dict = {}  # out_size -> [(position, request)]
+        pos, reqs = [], []
         for i, sp in enumerate(chunk):
             si = sset.index.get(sp.slide_id)
             if si is None:
                 res[i] = (None, LoaderError(f"no open slide for id {sp.slide_id!r}"))
                 continue
-            req = (si, sp.rect(), sp.target_mpp, sp.out_size)
-            try:
-                row = plan_specs([req], sset.records)[0]  # the reference's read_region checks, per spec
-                sset.slides[si].require_resident(row)
-            except Exception as exc:  # noqa: BLE001 - the error policy decides
-                res[i] = (None, exc)
+            pos.append(i)
+            reqs.append((si, sp.rect(), sp.target_mpp, sp.out_size))
+        errs: list = []
+        plan = plan_specs(reqs, sset.records, errors=errs)
+        bad = {}
+        for j, exc in errs:
+            bad[j] = exc
+        for j, row in enumerate(plan):
+            if j in bad:
                 continue
-            good.setdefault(sp.out_size, []).append((i, req))
-        for size, items in good.items():
-            arr = plan_specs([r for _, r in items], sset.records)
-            pix = sset.read_regions(arr, size).cpu().numpy()
-            for j, (i, _) in enumerate(items):
-                res[i] = (pix[j], None)
+            try:
+                sset.slides[int(row["slide"])].require_resident(row)
+            except Exception as exc:  # noqa: BLE001 - the error policy decides
+                bad[j] = exc
+        for j, exc in bad.items():
+            res[pos[j]] = (None, exc)
+        by_size: dict = {}
+        for j in range(len(reqs)):
+            if j not in bad:
+                by_size.setdefault(reqs[j][3], []).append(j)
+        for size, js in by_size.items():
+            pix = sset.read_regions(plan[js], size).cpu().numpy()
+            for k, j in enumerate(js):
+                res[pos[j]] = (pix[k], None)
         return res
 
     def gen():

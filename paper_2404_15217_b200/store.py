@@ -650,36 +650,48 @@ def ingest_image(pixels, slide_id: str, base_mpp: float, store_root, *, tile_siz
     return (rec, slide) if return_slide else rec
 
 
-def plan_specs(requests, records) -> np.ndarray:
+def plan_specs(requests, records, errors: list | None = None) -> np.ndarray:
     """Host read plan for explicit region requests.
 
     requests: iterable of (slide_index, (x, y, w, h), target_mpp, out_size).
     Validates bounds exactly like read_region/_read_window (pkg/store.py:667-702)
-    and fills level/side; sx/sy are filled on device (pf_plan_regions).
+    and fills level/side/sx/sy.  With ``errors`` (a list) a failing request does not raise:
+    ``(index, exception)`` is appended and its row is left zeroed (side 0).
     """
     reqs = list(requests)
     specs = np.zeros(len(reqs), dtype=N.SPEC_DTYPE)
     level_cache: dict = {}
     for i, (si, rect, mpp, out_size) in enumerate(reqs):
-        rec = records[si]
-        x, y, w, h = (int(v) for v in rect)
-        if out_size < 1:
-            raise ValueError("out_size must be >= 1")
-        if w < 1 or h < 1:
-            raise OutOfBoundsError("rect must have positive extent")
-        if x < 0 or y < 0 or x + w > rec.width or y + h > rec.height:
-            raise OutOfBoundsError(f"rect {tuple(rect)} outside level-0 bounds {rec.width}x{rec.height}")
-        key = (si, float(mpp))
-        if key not in level_cache:
-            level_cache[key] = select_level(rec, float(mpp))
-        li = level_cache[key]
-        lv = rec.levels[li]
-        side = max(1, round_half_away(out_size * mpp / lv.mpp))
-        sx, sy = round_half_away(x / lv.downsample), round_half_away(y / lv.downsample)
-        if sx < -1 or sy < -1 or sx + side > lv.width + 1 or sy + side > lv.height + 1:
-            raise OutOfBoundsError(f"window ({sx}, {sy}, {side}, {side}) outside level {li} ({lv.width}x{lv.height})")
-        specs[i] = (i, mpp, si, x, y, w, h, out_size, -1, li, side, sx, sy, 0)
+        if errors is not None:
+            try:
+                _plan_one(specs, i, si, rect, mpp, out_size, records, level_cache)
+            except Exception as exc:  # noqa: BLE001 - the caller's error policy decides
+                errors.append((i, exc))
+            continue
+        _plan_one(specs, i, si, rect, mpp, out_size, records, level_cache)
     return specs
+
+
+def _plan_one(specs, i, si, rect, mpp, out_size, records, level_cache):
+    """One request of plan_specs: read_region's checks (pkg/store.py:667-702), row i filled."""
+    rec = records[si]
+    x, y, w, h = (int(v) for v in rect)
+    if out_size < 1:
+        raise ValueError("out_size must be >= 1")
+    if w < 1 or h < 1:
+        raise OutOfBoundsError("rect must have positive extent")
+    if x < 0 or y < 0 or x + w > rec.width or y + h > rec.height:
+        raise OutOfBoundsError(f"rect {tuple(rect)} outside level-0 bounds {rec.width}x{rec.height}")
+    key = (si, float(mpp))
+    if key not in level_cache:
+        level_cache[key] = select_level(rec, float(mpp))
+    li = level_cache[key]
+    lv = rec.levels[li]
+    side = max(1, round_half_away(out_size * mpp / lv.mpp))
+    sx, sy = round_half_away(x / lv.downsample), round_half_away(y / lv.downsample)
+    if sx < -1 or sy < -1 or sx + side > lv.width + 1 or sy + side > lv.height + 1:
+        raise OutOfBoundsError(f"window ({sx}, {sy}, {side}, {side}) outside level {li} ({lv.width}x{lv.height})")
+    specs[i] = (i, mpp, si, x, y, w, h, out_size, -1, li, side, sx, sy, 0)
 
 
 _FITS: dict = {}
