@@ -65,7 +65,7 @@ __host__ __device__ inline SamplerWs carve_ws(void* ws, int n_slides, int window
 
 __host__ __device__ inline int64_t ws_bytes(int n_slides, int window) {
     return 256 + ((int64_t)n_slides * (window / 32) * 4 + 255) / 256 * 256 +
-           (int64_t)n_slides * window * 16 + (int64_t)window * 8;
+           (int64_t)n_slides * window * 16 + (int64_t)(window + 1) * 8;
 }
 
 // RandomStream.weighted_index (rng.py:88-103) given the stream draw u.
@@ -280,6 +280,12 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
     __shared__ int s_first, s_last;
     __shared__ int64_t s_seq0;  // stream seq at entry: warp 0 rewrites *state at exit
     WalkState w;
+#ifdef PF_WALK_TIMING  // phase timestamps into the workspace's reserved header (tools/walk_timing.py)
+#define PF_WT(i) do { if (threadIdx.x == 0) { uint64_t t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); reinterpret_cast<uint64_t*>(ws.reject_at)[1 + (i) + (finish ? 8 : 0)] = t_; } } while (0)
+#else
+#define PF_WT(i) ((void)0)
+#endif
+    PF_WT(0);
     load_ws(state, w);
     if (w.status != PF_OK || w.emitted >= n) return;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -298,6 +304,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
             bm_all = s_dyn;
         }
         __syncthreads();
+        PF_WT(1);
         // next_table: next accepted offset of every (slide, window offset) -- a parallel suffix
         // search over the accept bitmaps -- so each slide draw of the walk is one shared load.
         // Layout after the bitmaps: nextw[n_slides][words] (first non-zero word at or after w),
@@ -324,37 +331,51 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
             }
             __syncthreads();
             // entry (slide, a) = where a fresh draw starting at offset a leaves the walk:
-            //   f + 1            its first accepted attempt f (a spec),
+            //   f + 1            its first accepted attempt f (a spec); | 0x4000 when f + 1 reaches
+            //                    the window end (the walk's fast loop leaves on any flag bit),
             //   0x8000 | a + M   no accept within M = max_attempts (ExhaustedAttemptsError),
             //   0xffff           the window (or a rejected coords draw) ends inside the draw
             const int wlim_t = min(window, *ws.reject_at);
-            for (int sl = 0; sl < cfg.n_slides; ++sl)
-            for (int a = tid; a < window; a += kWalkThreads) {
-                const int i = sl * window + a;
+            // one thread per (slide, bitmap word): its 32 entries from the word in a register
+            for (int q = tid; q < cfg.n_slides * words; q += kWalkThreads) {
+                const int sl = q / words, wd = q - sl * words;
                 const uint32_t* bm = bm_all + (size_t)sl * words;
-                const int wd = a >> 5;
-                const uint32_t m = bm[wd] & (0xffffffffu << (a & 31));
-                int f = 0x7fffffff;
-                if (m) {
-                    f = wd * 32 + __ffs(m) - 1;
-                } else if (wd + 1 < words) {
+                const uint32_t word = bm[wd];
+                int f_next = 0x7fffffff;  // first accept after this word
+                if (wd + 1 < words) {
                     const int w2 = nextw[sl * words + wd + 1];
-                    if (w2 < words) f = w2 * 32 + __ffs(bm[w2]) - 1;
+                    if (w2 < words) f_next = w2 * 32 + __ffs(bm[w2]) - 1;
                 }
-                uint32_t e;
-                if (f < min(a + max_att, wlim_t)) e = (uint32_t)(f + 1);
-                else if (a + max_att <= wlim_t) e = 0x8000u | (uint32_t)(a + max_att);
-                else e = 0xffffu;
-                na[i] = (uint16_t)e;
+                uint32_t* dst = reinterpret_cast<uint32_t*>(na + (size_t)sl * window + wd * 32);  // window % 32 == 0
+#pragma unroll 4
+                for (int k = 0; k < 32; k += 2) {
+                    uint32_t pair = 0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int a = wd * 32 + k + h;
+                        const uint32_t m = word & (0xffffffffu << (k + h));
+                        const int f = m ? wd * 32 + __ffs(m) - 1 : f_next;
+                        uint32_t e;
+                        if (f < min(a + max_att, wlim_t)) e = (uint32_t)(f + 1) | (f + 1 >= wlim_t ? 0x4000u : 0u);
+                        else if (a + max_att <= wlim_t) e = 0x8000u | (uint32_t)(a + max_att);
+                        else e = 0xffffu;
+                        pair |= e << (16 * h);
+                    }
+                    dst[k >> 1] = pair;
+                }
             }
             __syncthreads();
         }
+        PF_WT(2);
         // fast walk: every slide draw of the call precomputed in parallel (no rejected draw among
         // them), then one thread runs the chain a -> next_accept(slide_j, a) + 1 whose only
         // dependent load per draw is the next-accept table; bookkeeping is off the chain
         // int32 entries: 16-bit ones get packed in pairs by the compiler, which then waits on the
         // prefetch load immediately
         int32_t* fdraw = reinterpret_cast<int32_t*>(na + (((size_t)cfg.n_slides * window + 1) & ~(size_t)1));
+        // the fast walk's emits, (slide << 16) | window offset, in shared memory (a global store per
+        // draw on the one-thread chain costs more than the chain itself)
+        int32_t* semit = fdraw + kFastDraws;
         __shared__ int s_fast;
         int n_fd = 0;
         if (next_table) {
@@ -384,8 +405,9 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
             }
             __syncthreads();
         }
+        PF_WT(3);
         if (next_table && s_fast) {
-            if (tid == 0) {
+            if (tid == 0) {  // one thread: no divergence bookkeeping inside the chain
                 const uint64_t m0 = w.c_mpp;
                 const int wlim = min(window, *ws.reject_at);
                 int a = 0, j = 0, emitted = w.emitted, used = 0;
@@ -402,7 +424,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                     for (int x = 0; x < span && f == 0x7fffffff; ++x)
                         if ((bm[x >> 5] >> (x & 31)) & 1u) f = x;
                     if (f != 0x7fffffff) {
-                        emit_list[emitted - s_first] = make_int2(s, f);
+                        semit[emitted - s_first] = (s << 16) | f;
                         ++emitted;
                         a = f + 1;
                         failures = 0;
@@ -417,39 +439,73 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                         mid_draw = true;
                     }
                 }
-                // the chain: one table load per draw, a = entry (the common case needs no ALU op);
-                // the next draw's slide and table row are known ahead
+                // The chain a <- entry(slide_j, a).  Fast loop for the common case (an accept below the
+                // window end, flag bits clear): table load, emit, next offset -- a handful of
+                // instructions per draw on one warp's dependent path; anything flagged (exhaustion,
+                // window end) or the last spec / last precomputed draw leaves to the general step.
                 if (!mid_draw && emitted < n && status == PF_OK && n_fd > 0) {
+                    // draws j+1 .. j+4 held in registers: each shared load has iterations to land
+                    // before the register rotation moves it (a move waits for its load)
                     int sj = fdraw[0];
-                    int s_nxt = fdraw[min(1, n_fd - 1)];
+                    int s_nxt = fdraw[min(1, n_fd - 1)], s_n2 = fdraw[min(2, n_fd - 1)];
+                    int s_n3 = fdraw[min(3, n_fd - 1)], s_n4 = fdraw[min(4, n_fd - 1)];
                     const uint16_t* row = na + (size_t)sj * window;
                     j = 1;
-                    while (true) {
-                        if (a >= wlim) {  // the window ends at this draw's first attempt
-                            s = sj, used = 0, mid_draw = true;
-                            break;
+                    if (a >= wlim) {  // the window ends at this draw's first attempt
+                        s = sj, used = 0, mid_draw = true;
+                    } else {
+                        const int n_left = n - emitted;
+                        int32_t* el = semit + (emitted - s_first);
+                        int k = 0;  // specs emitted by the fast loop
+                        while (true) {
+                            uint32_t e = row[a];
+                            const int last_j = n_fd - j;  // draws still precomputed after this one
+                            if (e < 0x4000u && k + 1 < n_left && last_j > 0) {  // plain accept, stream goes on
+                                el[k] = (sj << 16) | ((int)e - 1);
+                                ++k;
+                                a = (int)e;
+                                failures = 0;
+                                sj = s_nxt;
+                                row = na + (size_t)sj * window;
+                                ++j;
+                                s_nxt = s_n2, s_n2 = s_n3, s_n3 = s_n4;
+                                s_n4 = fdraw[min(j + 3, n_fd - 1)];
+                                continue;
+                            }
+                            // general step for this draw
+                            emitted += k;
+                            el += k;
+                            k = 0;
+                            e &= (e == 0xffffu || (e & 0x8000u)) ? 0xffffu : 0x3fffu;  // drop the 0x4000 mark
+                            const bool acc = e < 0x8000u, win = e == 0xffffu;
+                            if (acc) {
+                                PF_CHECK(emitted - s_first < window);
+                                semit[emitted - s_first] = (sj << 16) | ((int)e - 1);
+                                ++emitted;
+                                failures = 0;
+                                a = (int)e;
+                            } else if (!win) {
+                                a = (int)(e & 0x7fffu);
+                                if (++failures >= flimit) status = PF_ERR_NO_SAMPLABLE;
+                            } else {  // the window ends inside this draw
+                                used = wlim - a;
+                                a = wlim;
+                                s = sj, mid_draw = true;
+                                break;
+                            }
+                            if (emitted >= n || status != PF_OK || j == n_fd) break;
+                            if (a >= wlim) {  // the next draw starts at the window end
+                                s = s_nxt, used = 0, mid_draw = true;
+                                ++j;
+                                break;
+                            }
+                            el = semit + (emitted - s_first);
+                            sj = s_nxt;
+                            row = na + (size_t)sj * window;
+                            ++j;
+                            s_nxt = s_n2, s_n2 = s_n3, s_n3 = s_n4;
+                            s_n4 = fdraw[min(j + 3, n_fd - 1)];
                         }
-                        const uint32_t e = row[a];
-                        if (e < 0x8000u) {  // accepted at e - 1
-                            PF_CHECK(emitted - s_first < window);
-                            emit_list[emitted - s_first] = make_int2(sj, (int)e - 1);
-                            ++emitted;
-                            a = (int)e;
-                            failures = 0;
-                        } else if (e != 0xffffu) {  // exhausted
-                            a = (int)(e & 0x7fffu);
-                            if (++failures >= flimit) status = PF_ERR_NO_SAMPLABLE;
-                        } else {  // the window ends inside this draw
-                            used = wlim - a;
-                            a = wlim;
-                            s = sj, mid_draw = true;
-                            break;
-                        }
-                        if (emitted >= n || status != PF_OK || j == n_fd) break;  // j == n_fd: next round
-                        sj = s_nxt;
-                        row = na + (size_t)sj * window;
-                        ++j;
-                        s_nxt = fdraw[min(j, n_fd - 1)];
                     }
                 }
                 if (!mid_draw) used = 0;
@@ -572,15 +628,24 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
             if (lane == 0) s_last = w.emitted;
         }
         __syncthreads();
+        PF_WT(4);
         // materialise the emitted specs in parallel
         const int first = s_first, last = s_last;
         const int64_t seq0 = s_seq0;
+        const bool fast_emits = next_table && s_fast;
         for (int i = first + tid; i < last; i += kWalkThreads) {
-            const int2 e = emit_list[i - first];
+            int2 e;
+            if (fast_emits) {
+                const int v = semit[i - first];
+                e = make_int2(v >> 16, v & 0xffff);
+            } else {
+                e = emit_list[i - first];
+            }
             const int4 cd = ws.cands[(size_t)e.x * window + e.y];
             emit_spec(cfg, slides[e.x], descs[e.x], e.x, cd.x, cd.y, cd.z, seq0 + (i - first), out + i);
         }
     }
+    PF_WT(5);
     if (tid >= 32) return;
     if (finish) {
         uint32_t* sm = s_dyn;
@@ -695,7 +760,7 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     const int bm_in_smem = rounds > 0 && bm_bytes_all <= 160 * 1024;
     // next-accepted-offset table beside the bitmaps (uint16 offsets: window < 0xffff)
     const size_t nt_bytes = bm_bytes_all + ((size_t)cfg->n_slides * (window / 32) + 1) / 2 * 4 +
-                            ((size_t)cfg->n_slides * window + 1) / 2 * 4 + (size_t)kFastDraws * 4;
+                            ((size_t)cfg->n_slides * window + 1) / 2 * 4 + (size_t)kFastDraws * 4 + (size_t)window * 4;
     const int next_table = bm_in_smem && window + cfg->max_attempts < 0x7fff && nt_bytes <= 200 * 1024;
     const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid),
                                       next_table ? nt_bytes : (bm_in_smem ? bm_bytes_all : (size_t)0));
