@@ -458,20 +458,26 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                         int32_t* el = semit + (emitted - s_first);
                         int k = 0;  // specs emitted by the fast loop
                         while (true) {
-                            uint32_t e = row[a];
-                            const int last_j = n_fd - j;  // draws still precomputed after this one
-                            if (e < 0x4000u && k + 1 < n_left && last_j > 0) {  // plain accept, stream goes on
-                                el[k] = (sj << 16) | ((int)e - 1);
-                                ++k;
-                                a = (int)e;
-                                failures = 0;
-                                sj = s_nxt;
-                                row = na + (size_t)sj * window;
-                                ++j;
-                                s_nxt = s_n2, s_n2 = s_n3, s_n3 = s_n4;
-                                s_n4 = fdraw[min(j + 3, n_fd - 1)];
-                                continue;
+                            uint32_t e;
+                            // plain accepts while the stream goes on, eight per back edge (a taken
+                            // branch per draw costs as much as the draw on one warp)
+#define PF_FAST_DRAW                                                                            \
+    e = row[a];                                                                                 \
+    if (!(e < 0x4000u && k + 1 < n_left && j < n_fd)) break;                                    \
+    el[k] = (sj << 16) | ((int)e - 1);                                                          \
+    ++k;                                                                                        \
+    a = (int)e;                                                                                 \
+    sj = s_nxt;                                                                                 \
+    row = na + (size_t)sj * window;                                                             \
+    ++j;                                                                                        \
+    s_nxt = s_n2, s_n2 = s_n3, s_n3 = s_n4;                                                     \
+    s_n4 = fdraw[min(j + 3, n_fd - 1)];
+                            for (;;) {
+                                PF_FAST_DRAW PF_FAST_DRAW PF_FAST_DRAW PF_FAST_DRAW
+                                PF_FAST_DRAW PF_FAST_DRAW PF_FAST_DRAW PF_FAST_DRAW
                             }
+#undef PF_FAST_DRAW
+                            if (k > 0) failures = 0;
                             // general step for this draw
                             emitted += k;
                             el += k;
