@@ -235,8 +235,8 @@ class Feed:
 
 
 def make_feed(args, pf, plan, slides, rank, src_size=224, n_local=8, patch=224):
-    # speculation rounds per sampler call (the loaders' default, 2; PF_SAMPLER_ROUNDS for experiments)
-    rounds = int(os.environ.get("PF_SAMPLER_ROUNDS", "2"))
+    # speculation rounds per sampler call (the loaders' default, 1; PF_SAMPLER_ROUNDS for experiments)
+    rounds = int(os.environ.get("PF_SAMPLER_ROUNDS", "1"))
     from paper_2404_15217_b200.multicrop import MultiCropConfig, MultiCropLoader
     from paper_2404_15217_b200.pipeline import RegionLoader
 

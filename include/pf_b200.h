@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 2
+#define PF_ABI_VERSION 3
 #define PF_MAX_LEVELS 12
 #define PF_MAX_MPPS 8
 #define PF_MAX_CROPS 16
@@ -286,6 +286,19 @@ int pf_polygon_index_size(const double* xy, const int64_t* ring_off, int32_t n_r
 int pf_polygon_index_build(const double* xy, const int64_t* ring_off, int32_t n_rings, void* blob,
                            int64_t bytes);
 
+/* Coarse classification raster of a polygon for the sampler's acceptance test
+ * (no reference counterpart: a precomputed filter in front of overlap_fraction,
+ * pkg/foreground.py:246-286).  Square cells of `cell` px (a power of two >= 8)
+ * covering the bounding box plus one cell; each cell is 2 bits: 01 every point
+ * of the cell (closed, grown by 1 px) is inside, 00 every point outside, 1x an
+ * edge comes within 1 px of it.  A window whose cells are all 01 (all 00) has
+ * overlap_fraction 1.0 (0.0) exactly, since the even-odd parity is constant over
+ * an edge-free region.  DEVICE blob and output; _bytes sizes the output from
+ * the polygon's bbox (ForegroundPolygon.bounding_box()). */
+int pf_polygon_raster_bytes(const double* bbox, double cell, int64_t* bytes);
+int pf_polygon_raster_build(const void* poly_blob_dev, const double* bbox, double cell, void* raster_dev,
+                            int64_t raster_bytes, void* stream);
+
 /* Batched overlap_fraction (pkg/foreground.py:246-286, points_in_polygon
  * 223-243): rects_dev is n x (x, y, w, h) float64; bit-exact FP64 even-odd
  * test on the (grid+1)^2 corners + grid^2 centres.  32 <= grid <= 256. */
@@ -320,6 +333,8 @@ typedef struct pf_sampler_slide {
     int32_t level[PF_MAX_MPPS]; /* read plan per mpp: select_level */
     int32_t side[PF_MAX_MPPS];
     int32_t _pad;
+    uint64_t raster;    /* device address of a pf_polygon_raster_build raster of poly_blob, or 0
+                           (ABI 3; candidates it classifies skip the lattice test) */
 } pf_sampler_slide;
 
 /* Device-resident stream state: the reference's StreamSet counters plus the

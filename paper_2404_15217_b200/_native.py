@@ -91,6 +91,7 @@ class SamplerSlide(C.Structure):
         ("level", C.c_int32 * PF_MAX_MPPS),
         ("side", C.c_int32 * PF_MAX_MPPS),
         ("_pad", C.c_int32),
+        ("raster", C.c_uint64),
     ]
 
 
@@ -208,6 +209,8 @@ class _Lib:
             "pf_polygon_index_size": ([vp, vp, i32, C.POINTER(i64)], C.c_int),
             "pf_polygon_index_build": ([vp, vp, i32, vp, i64], C.c_int),
             "pf_overlap_fraction": ([vp, vp, i32, i32, vp, vp], C.c_int),
+            "pf_polygon_raster_bytes": ([vp, dbl, C.POINTER(i64)], C.c_int),
+            "pf_polygon_raster_build": ([vp, vp, dbl, vp, i64, vp], C.c_int),
             "pf_sample_workspace_bytes": ([C.POINTER(SamplerConfig), i32, C.POINTER(i64)], C.c_int),
             "pf_sample": (
                 [C.POINTER(SamplerConfig), vp, vp, vp, i32, vp, vp, i64, i32, i32, i32, vp],
@@ -234,7 +237,7 @@ class _Lib:
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res
-        if L.pf_abi_version() != 2:
+        if L.pf_abi_version() != 3:
             raise errors.NativeLibraryError("libpfb200 ABI version mismatch")
 
     @classmethod

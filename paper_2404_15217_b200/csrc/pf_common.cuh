@@ -108,4 +108,28 @@ __host__ __device__ __forceinline__ bool randrange_accepts(uint64_t v, uint64_t 
     return limit == 0ull || v < limit;
 }
 
+// randrange_accepts(v, randrange_limit(n)) without the 64-bit division on the common path:
+// limit = 2^64 - (2^64 mod n) > 2^64 - n, so v < 2^64 - n accepts outright; only a draw in
+// the top n values (probability n / 2^64) computes the exact limit.
+__device__ __forceinline__ bool randrange_accepts_n(uint64_t v, uint64_t n) {
+    return v < 0ull - n || randrange_accepts(v, randrange_limit(n));
+}
+
+// v % n (1 <= n < 2^50) without the 64-bit division subroutine: two FP64 quotient estimates
+// and one exact correction.  Pass 1: q = trunc(rz(v) * rn(1/n)) is within 3*2^-52*v/n + 1 of
+// v/n, so r1 = v - q*n (exact in wrapping arithmetic) has |r1| <= 3*2^12 + n.  Pass 2:
+// rn(r1 * rn(1/n)) is within 2^-40 of r1/n, so its floor is floor(r1/n) or one off when r1/n
+// is that close to an integer, and r2 = r1 - floor(.)*n lies in [-n, 2n).  (Written as loops,
+// the correction is turned into a division by the compiler.)
+__device__ __forceinline__ uint64_t mod_u64(uint64_t v, uint64_t n) {
+    if (n >= (1ull << 50)) return v % n;
+    const double inv = __drcp_rn((double)n);
+    const uint64_t q = __double2ull_rz(__dmul_rn(__ull2double_rz(v), inv));
+    int64_t r = (int64_t)(v - q * n);
+    r -= __double2ll_rd(__dmul_rn((double)r, inv)) * (int64_t)n;
+    if (r < 0) r += (int64_t)n;
+    else if (r >= (int64_t)n) r -= (int64_t)n;
+    return (uint64_t)r;
+}
+
 }  // namespace pf

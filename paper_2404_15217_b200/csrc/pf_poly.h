@@ -23,6 +23,16 @@ struct PolyHeader {
 
 constexpr int32_t kPolyMagic = 0x50464231;  // "PFB1"
 
+// Classification raster (pf_polygon_raster_build): header | uint32 words[ny][pitch], 16
+// cells of 2 bits per word (cell c of a row at bits 2(c%16), 2(c%16)+1 of word c/16).
+struct RasterHeader {
+    double ox, oy, cell, inv_cell;  // cell (i, j) covers [ox + i*cell, ox + (i+1)*cell) x ...
+    int32_t nx, ny, pitch, magic;
+    int64_t _reserved[2];
+};
+constexpr int32_t kRasterMagic = 0x50465231;  // "PFR1"
+constexpr uint32_t kRasterInside = 0x55555555u;
+
 inline int64_t align16(int64_t v) { return (v + 15) & ~int64_t(15); }
 
 }  // namespace pf

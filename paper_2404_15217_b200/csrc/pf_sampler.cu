@@ -43,10 +43,18 @@ __global__ void overlap_kernel(const void* blob, const double* rects, int n, int
 // ---------------------------------------------------------------------------
 // Sampler helpers (pkg/rng.py, pkg/sampler.py)
 // ---------------------------------------------------------------------------
+constexpr int kFastDraws = 8192;  // slide draws precomputed per fast walk (int32)
+
 struct SamplerWs {
     uint32_t* bitmaps;  // [n_slides][window/32]
     int4* cands;        // [n_slides][window]: x, y, mpp_idx, -
     int32_t* reject_at; // first window offset whose coords draws were rejected
+    int32_t* n_queue;   // kCountBase + candidates queued for the overlap test this round
+    int32_t* queue;     // [n_slides * window]: candidates the raster left undecided
+    int2* acc;          // [n_slides * window]: per queued candidate (covered cells, parts done)
+    uint16_t* na;       // [n_slides * window]: next-accept table (sample_table_kernel)
+    int32_t* fdraw;     // [kFastDraws]: the call's slide draws (sample_table_kernel)
+    int32_t* draws_ok;  // kCountBase unless a precomputed slide draw was rejected
     int2* emits;        // [window]: (slide, window offset) of specs emitted by the walk
 };
 
@@ -54,18 +62,29 @@ __host__ __device__ inline SamplerWs carve_ws(void* ws, int n_slides, int window
     SamplerWs w;
     uint8_t* p = reinterpret_cast<uint8_t*>(ws);
     w.reject_at = reinterpret_cast<int32_t*>(p);
+    w.n_queue = reinterpret_cast<int32_t*>(p + 4);
+    w.draws_ok = reinterpret_cast<int32_t*>(p + 8);  // PF_WALK_TIMING stamps start at byte 32
     p += 256;
     w.bitmaps = reinterpret_cast<uint32_t*>(p);
     p += (((size_t)n_slides * (window / 32) * 4) + 255) / 256 * 256;
     w.cands = reinterpret_cast<int4*>(p);
     p += (size_t)n_slides * window * 16;
+    w.queue = reinterpret_cast<int32_t*>(p);
+    p += (size_t)n_slides * window * 4;
+    w.acc = reinterpret_cast<int2*>(p);
+    p += (size_t)n_slides * window * 8;
+    w.fdraw = reinterpret_cast<int32_t*>(p);
+    p += (size_t)kFastDraws * 4;
+    w.na = reinterpret_cast<uint16_t*>(p);
+    p += ((size_t)n_slides * window * 2 + 15) / 16 * 16;
     w.emits = reinterpret_cast<int2*>(p);
     return w;
 }
 
 __host__ __device__ inline int64_t ws_bytes(int n_slides, int window) {
     return 256 + ((int64_t)n_slides * (window / 32) * 4 + 255) / 256 * 256 +
-           (int64_t)n_slides * window * 16 + (int64_t)(window + 1) * 8;
+           (int64_t)n_slides * window * 28 + (int64_t)kFastDraws * 4 + ((int64_t)n_slides * window * 2 + 15) / 16 * 16 +
+           (int64_t)(window + 1) * 8;
 }
 
 // RandomStream.weighted_index (rng.py:88-103) given the stream draw u.
@@ -120,42 +139,216 @@ __device__ __forceinline__ void emit_spec(const pf_sampler_config& cfg, const pf
 }
 
 // ---------------------------------------------------------------------------
-// Speculative evaluation: one warp per (slide, window offset).
+// Speculative evaluation of every (slide, window offset) candidate, in two passes.
+//
+// sample_classify_kernel, a thread per candidate: the mpp and coordinate draws, then bounds
+// on the window's covered-cell count from the slide's classification raster (pf_raster.cu):
+// lattice cells inside clean-inside raster cells are covered, inside clean-outside ones not.
+// When the bounds settle "count >= need" the candidate is decided on the spot (its bitmap bit
+// set or not); the rest are queued.
+//
+// sample_eval_kernel, kEvalParts warps per queued candidate, each counting a quarter of its
+// lattice cell rows (pf_poly.cuh warp_overlap_count_rows); the last part to finish compares
+// the total with the threshold.  One resident grid (few large blocks: the block launch ramp of
+// ~2000 small ones cost ~10 us) strides the parts over its warps.  Only windows near the
+// tissue border reach this pass (~2 % of the candidates), so it is short, and splitting them
+// keeps its length at a fraction of one window's latency.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(64, 16) sample_eval_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
-                                   const pf_sampler_state* state, SamplerWs ws, int window, int n,
-                                   EvalConsts k) {
-    extern __shared__ __align__(16) uint32_t s_masks[];
+constexpr int kEvalWarps = 8;
+#ifndef PF_EVAL_MIN_BLOCKS
+#define PF_EVAL_MIN_BLOCKS 4
+#endif
+constexpr int32_t kCountBase = 0x7f7f7f7f;  // the round's memset value of reject_at / n_queue
+constexpr int kEvalParts = 4;  // a queued window's cell rows are counted by this many warps
+
+__global__ void __launch_bounds__(256) sample_classify_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
+                                                              const pf_sampler_state* state, SamplerWs ws, int window,
+                                                              int n, EvalConsts k) {
     if (state->status != PF_OK || state->emitted >= n) return;
-    const int warp_in_block = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const uint32_t q = blockIdx.x * (blockDim.x >> 5) + warp_in_block;  // n_slides * window < 2^31 (host)
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (uint32_t)cfg.n_slides * (uint32_t)window) return;
     const int s = (int)(q / (uint32_t)window), a = (int)(q % (uint32_t)window);
     const pf_sampler_slide& sl = slides[s];
     const uint64_t m0 = state->c_mpp, c0 = state->c_coords;
     const int mi = weighted_pick(stream_u64(cfg.key_mpp, m0 + (uint64_t)a + 1), cfg.mpp_weight, cfg.n_mpps,
                                  k.weight_total);
-    const int fp = sl.fp[mi];
     const uint64_t nx = (uint64_t)(sl.x_hi[mi] - sl.x_lo[mi] + 1);
     const uint64_t ny = (uint64_t)(sl.y_hi[mi] - sl.y_lo[mi] + 1);
     const uint64_t vx = stream_u64(cfg.key_coords, c0 + 2ull * (uint64_t)a + 1);
     const uint64_t vy = stream_u64(cfg.key_coords, c0 + 2ull * (uint64_t)a + 2);
-    const bool rejected = !randrange_accepts(vx, randrange_limit(nx)) || !randrange_accepts(vy, randrange_limit(ny));
-    if (rejected) {
-        if (lane == 0) atomicMin(ws.reject_at, a);
+    if (!randrange_accepts_n(vx, nx) || !randrange_accepts_n(vy, ny)) {
+        atomicMin(ws.reject_at, a);
         return;
     }
-    const int x = sl.x_lo[mi] + (int)(vx % nx);
-    const int y = sl.y_lo[mi] + (int)(vy % ny);
+    const int x = sl.x_lo[mi] + (int)mod_u64(vx, nx);
+    const int y = sl.y_lo[mi] + (int)mod_u64(vy, ny);
+    const int fp = sl.fp[mi];
+    ws.cands[q] = make_int4(x, y, mi, 0);
+    int lo = 0, hi = cfg.grid * cfg.grid;
+    if (sl.raster)
+        raster_bounds_thread(reinterpret_cast<const RasterHeader*>(sl.raster), (double)x, (double)y, (double)fp,
+                             cfg.grid, lo, hi);
+    if (lo >= k.need || hi < k.need) {  // decided by the bounds on the covered-cell count
+        if (lo >= k.need) atomicOr(ws.bitmaps + (size_t)s * (window / 32) + (a >> 5), 1u << (a & 31));
+    } else {
+        const uint32_t at = atomicAdd(reinterpret_cast<unsigned*>(ws.n_queue), 1u) - (uint32_t)kCountBase;
+        ws.queue[at] = (int)q;
+        ws.acc[at] = make_int2(0, 0);
+    }
+}
+
+// One part of a queued candidate: the covered cells of cell rows [part, part + 1) * grid /
+// kEvalParts, added to the candidate's total; the part that completes it sets the bit.
+__device__ __forceinline__ void eval_part(const pf_sampler_config& cfg, const pf_sampler_slide* slides,
+                                          const SamplerWs& ws, int window, const EvalConsts& k, uint32_t item,
+                                          uint32_t* sm) {
+    const int lane = threadIdx.x & 31;
+#ifdef PF_EVAL_TIMING
+    uint64_t t_0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_0));
+#endif
+    const uint32_t at = item / kEvalParts;
+    const int part = (int)(item % kEvalParts);
+    const uint32_t q = (uint32_t)__ldg(ws.queue + at);
+    const int s = (int)(q / (uint32_t)window), a = (int)(q % (uint32_t)window);
+    const pf_sampler_slide& sl = slides[s];
+    const int4 cd = ws.cands[q];
+    const int fp = sl.fp[cd.z];
     const PolyView P = poly_view(reinterpret_cast<const void*>(sl.poly_blob));
-    uint32_t* sm = s_masks + warp_in_block * (overlap_smem_bytes_chunked(cfg.grid) / 4);
-    const bool accept = warp_overlap_accept(P, (double)x, (double)y, (double)fp, (double)fp, cfg.grid, sm,
-                                            cfg.min_foreground, k.need);
+    const int r_lo = part * cfg.grid / kEvalParts, r_hi = (part + 1) * cfg.grid / kEvalParts;
+    const int c = warp_overlap_count_rows(P, (double)cd.x, (double)cd.y, (double)fp, cfg.grid, sm, r_lo, r_hi);
     if (lane == 0) {
-        ws.cands[(size_t)s * window + a] = make_int4(x, y, mi, 0);
-        if (accept)
-            atomicOr(ws.bitmaps + (size_t)s * (window / 32) + (a >> 5), 1u << (a & 31));
+        atomicAdd(&ws.acc[at].x, c);
+        __threadfence();
+        if (atomicAdd(&ws.acc[at].y, 1) == kEvalParts - 1) {
+            const int total = atomicAdd(&ws.acc[at].x, 0);
+            if (total >= k.need) atomicOr(ws.bitmaps + (size_t)s * (window / 32) + (a >> 5), 1u << (a & 31));
+        }
+#ifdef PF_EVAL_TIMING
+        uint64_t t_1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_1));
+        atomicMax(reinterpret_cast<unsigned long long*>(ws.reject_at) + 21, (unsigned long long)t_1);
+        // part latency (ns) and start offset into the unused tail of the queue array
+        if (item < 8192) {
+            ws.queue[16384 + 2 * item] = (int)(t_1 - t_0);
+            ws.queue[16384 + 2 * item + 1] = (int)(t_0 & 0x7fffffff);
+        }
+#endif
+    }
+}
+
+__global__ void __launch_bounds__(kEvalWarps * 32, PF_EVAL_MIN_BLOCKS) sample_eval_kernel(pf_sampler_config cfg,
+                                   const pf_sampler_slide* slides, const pf_sampler_state* state, SamplerWs ws,
+                                   int window, int n, EvalConsts k) {
+    extern __shared__ __align__(16) uint32_t s_masks[];
+    if (state->status != PF_OK || state->emitted >= n) return;
+    const int lane = threadIdx.x & 31;
+#ifdef PF_EVAL_TIMING  // warp-pass span (tools/eval_timing.py)
+    if (lane == 0) {
+        uint64_t t_0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_0));
+        atomicMin(reinterpret_cast<unsigned long long*>(ws.reject_at) + 20, (unsigned long long)t_0);
+    }
+#endif
+    // queue complete (stream order); every queued candidate is kEvalParts work items of about
+    // equal cost, strided over the resident warps (no claim counter to contend on)
+    const uint32_t total = ((uint32_t)*ws.n_queue - (uint32_t)kCountBase) * kEvalParts;
+    uint32_t* sm = s_masks + (threadIdx.x >> 5) * (overlap_smem_bytes_chunked(cfg.grid) / 4);
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < total; i += nwarps)
+        eval_part(cfg, slides, ws, window, k, i, sm);
+}
+
+// ---------------------------------------------------------------------------
+// Next-accept table and slide draws for the walk, on many CTAs (the walk is one CTA: built
+// there, the table alone took ~8 us of it).  Blocks [0, n_slides): one slide's table; the
+// rest: the call's slide draws.
+//
+// entry (slide, a) = where a fresh draw starting at offset a leaves the walk:
+//   f + 1            its first accepted attempt f (a spec); | 0x4000 when f + 1 reaches the
+//                    window end (the walk's fast loop leaves on any flag bit),
+//   0x8000 | a + M   no accept within M = max_attempts (ExhaustedAttemptsError),
+//   0xffff           the window (or a rejected coords draw) ends inside the draw
+// ---------------------------------------------------------------------------
+constexpr int kTableThreads = 512;
+
+__global__ void __launch_bounds__(kTableThreads) sample_table_kernel(pf_sampler_config cfg,
+                                                                     const pf_sampler_slide* slides,
+                                                                     const pf_sampler_state* state, SamplerWs ws,
+                                                                     int window, int n) {
+    __shared__ uint32_t s_bm[2048];   // window <= 65536
+    __shared__ uint16_t s_next[2048];  // first non-zero word at or after w
+    if (state->status != PF_OK || state->emitted >= n) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int words = window / 32;
+    if ((int)blockIdx.x >= cfg.n_slides) {  // slide draws (sample_slide, sampler.py:130-137)
+        const int n_fd = min(kFastDraws, 2 * (n - state->emitted) + 256);
+        const int i = ((int)blockIdx.x - cfg.n_slides) * kTableThreads + tid;
+        if (i >= n_fd) return;
+        const uint64_t v = stream_u64(cfg.key_slide, state->c_slide + 1 + (uint64_t)i);
+        int sidx;
+        if (cfg.strategy == 0) {
+            const uint64_t nn = (uint64_t)cfg.n_slides;
+            sidx = randrange_accepts(v, randrange_limit(nn)) ? (int)(v % nn) : -1;
+        } else {
+            double total = 0.0;
+            for (int k = 0; k < cfg.n_slides; ++k) total = __dadd_rn(total, slides[k].weight);
+            const double u = __dadd_rn(0.0, __dmul_rn(u64_to_unit(v), __dsub_rn(total, 0.0)));
+            double acc = 0.0;
+            sidx = cfg.n_slides - 1;
+            for (int k = 0; k < cfg.n_slides; ++k) {
+                acc = __dadd_rn(acc, slides[k].weight);
+                if (u < acc) {
+                    sidx = k;
+                    break;
+                }
+            }
+        }
+        if (sidx < 0) *ws.draws_ok = 0;  // a rejected draw (p ~ n / 2^64): the general walk handles it
+        ws.fdraw[i] = sidx;
+        return;
+    }
+    const int sl = blockIdx.x;
+    const uint32_t* bm = ws.bitmaps + (size_t)sl * words;
+    for (int i = tid; i < words; i += kTableThreads) s_bm[i] = bm[i];
+    __syncthreads();
+    if (tid < 32) {  // suffix min of the non-zero word indices, 32 words per step from the end
+        int carry = words;
+        for (int base = ((words - 1) >> 5) << 5; base >= 0; base -= 32) {
+            const int wi = base + lane;
+            int v = (wi < words && s_bm[wi] != 0u) ? wi : words;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_down_sync(0xffffffffu, v, o);
+                if (lane + o < 32) v = min(v, u);
+            }
+            v = min(v, carry);
+            if (wi < words) s_next[wi] = (uint16_t)v;
+            carry = __shfl_sync(0xffffffffu, v, 0);
+        }
+    }
+    __syncthreads();
+    const int max_att = cfg.max_attempts;
+    const int wlim_t = min(window, *ws.reject_at);
+    uint16_t* na = ws.na + (size_t)sl * window;
+    for (int a = tid; a < window; a += kTableThreads) {  // consecutive threads, consecutive entries
+        const int wd = a >> 5;
+        const uint32_t m = s_bm[wd] & (0xffffffffu << (a & 31));
+        int f;
+        if (m) {
+            f = wd * 32 + __ffs(m) - 1;
+        } else {
+            f = 0x7fffffff;  // first accept after this word
+            if (wd + 1 < words) {
+                const int w2 = s_next[wd + 1];
+                if (w2 < words) f = w2 * 32 + __ffs(s_bm[w2]) - 1;
+            }
+        }
+        uint32_t e;
+        if (f < min(a + max_att, wlim_t)) e = (uint32_t)(f + 1) | (f + 1 >= wlim_t ? 0x4000u : 0u);
+        else if (a + max_att <= wlim_t) e = 0x8000u | (uint32_t)(a + max_att);
+        else e = 0xffffu;
+        na[a] = (uint16_t)e;
     }
 }
 
@@ -263,7 +456,6 @@ __device__ inline int slow_attempt(const pf_sampler_config& cfg, const pf_sample
 // block.  The exact sequential path finishes whatever the table cannot decide.
 constexpr int kWalkThreads = 512;
 constexpr int kDrawCache = 256;
-constexpr int kFastDraws = 8192;  // slide draws precomputed per fast walk (int32 in shared memory)
 
 __device__ inline double k_total_weight(const pf_sampler_config& cfg, const pf_sampler_slide* slides) {
     double total = 0.0;
@@ -281,7 +473,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
     __shared__ int64_t s_seq0;  // stream seq at entry: warp 0 rewrites *state at exit
     WalkState w;
 #ifdef PF_WALK_TIMING  // phase timestamps into the workspace's reserved header (tools/walk_timing.py)
-#define PF_WT(i) do { if (threadIdx.x == 0) { uint64_t t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); reinterpret_cast<uint64_t*>(ws.reject_at)[1 + (i) + (finish ? 8 : 0)] = t_; } } while (0)
+#define PF_WT(i) do { if (threadIdx.x == 0) { uint64_t t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); reinterpret_cast<uint64_t*>(ws.reject_at)[4 + (i) + (finish ? 8 : 0)] = t_; } } while (0)
 #else
 #define PF_WT(i) ((void)0)
 #endif
@@ -305,72 +497,13 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
         }
         __syncthreads();
         PF_WT(1);
-        // next_table: next accepted offset of every (slide, window offset) -- a parallel suffix
-        // search over the accept bitmaps -- so each slide draw of the walk is one shared load.
-        // Layout after the bitmaps: nextw[n_slides][words] (first non-zero word at or after w),
-        // na[n_slides][window] (uint16; 0xffff = none).
+        // next_table (sample_table_kernel, many CTAs): entry (slide, a) of the next-accept table
+        // and the call's slide draws, copied next to the bitmaps.  Layout after the bitmaps:
+        // [n_slides * words uint16 (unused)] na[n_slides][window] (uint16) fdraw[kFastDraws]
+        // semit[...]
         uint16_t* nextw = reinterpret_cast<uint16_t*>(s_dyn + cfg.n_slides * words);
         uint16_t* na = nextw + ((cfg.n_slides * words + 1) & ~1);
-        if (next_table) {
-            const int warp = tid >> 5, nwarps = kWalkThreads / 32;
-            for (int sl = warp; sl < cfg.n_slides; sl += nwarps) {  // one warp per slide, chunks from the end
-                const uint32_t* bm = bm_all + (size_t)sl * words;
-                int carry = words;
-                for (int base = ((words - 1) >> 5) << 5; base >= 0; base -= 32) {
-                    const int wi = base + lane;
-                    int v = (wi < words && bm[wi] != 0u) ? wi : words;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int u = __shfl_down_sync(0xffffffffu, v, o);
-                        if (lane + o < 32) v = min(v, u);
-                    }
-                    v = min(v, carry);
-                    if (wi < words) nextw[sl * words + wi] = (uint16_t)v;
-                    carry = __shfl_sync(0xffffffffu, v, 0);
-                }
-            }
-            __syncthreads();
-            // entry (slide, a) = where a fresh draw starting at offset a leaves the walk:
-            //   f + 1            its first accepted attempt f (a spec); | 0x4000 when f + 1 reaches
-            //                    the window end (the walk's fast loop leaves on any flag bit),
-            //   0x8000 | a + M   no accept within M = max_attempts (ExhaustedAttemptsError),
-            //   0xffff           the window (or a rejected coords draw) ends inside the draw
-            const int wlim_t = min(window, *ws.reject_at);
-            // one thread per (slide, bitmap word): its 32 entries from the word in a register
-            for (int q = tid; q < cfg.n_slides * words; q += kWalkThreads) {
-                const int sl = q / words, wd = q - sl * words;
-                const uint32_t* bm = bm_all + (size_t)sl * words;
-                const uint32_t word = bm[wd];
-                int f_next = 0x7fffffff;  // first accept after this word
-                if (wd + 1 < words) {
-                    const int w2 = nextw[sl * words + wd + 1];
-                    if (w2 < words) f_next = w2 * 32 + __ffs(bm[w2]) - 1;
-                }
-                uint32_t* dst = reinterpret_cast<uint32_t*>(na + (size_t)sl * window + wd * 32);  // window % 32 == 0
-#pragma unroll 4
-                for (int k = 0; k < 32; k += 2) {
-                    uint32_t pair = 0;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int a = wd * 32 + k + h;
-                        const uint32_t m = word & (0xffffffffu << (k + h));
-                        const int f = m ? wd * 32 + __ffs(m) - 1 : f_next;
-                        uint32_t e;
-                        if (f < min(a + max_att, wlim_t)) e = (uint32_t)(f + 1) | (f + 1 >= wlim_t ? 0x4000u : 0u);
-                        else if (a + max_att <= wlim_t) e = 0x8000u | (uint32_t)(a + max_att);
-                        else e = 0xffffu;
-                        pair |= e << (16 * h);
-                    }
-                    dst[k >> 1] = pair;
-                }
-            }
-            __syncthreads();
-        }
-        PF_WT(2);
-        // fast walk: every slide draw of the call precomputed in parallel (no rejected draw among
-        // them), then one thread runs the chain a -> next_accept(slide_j, a) + 1 whose only
-        // dependent load per draw is the next-accept table; bookkeeping is off the chain
-        // int32 entries: 16-bit ones get packed in pairs by the compiler, which then waits on the
+        // int32 draws: 16-bit ones get packed in pairs by the compiler, which then waits on the
         // prefetch load immediately
         int32_t* fdraw = reinterpret_cast<int32_t*>(na + (((size_t)cfg.n_slides * window + 1) & ~(size_t)1));
         // the fast walk's emits, (slide << 16) | window offset, in shared memory (a global store per
@@ -380,31 +513,23 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
         int n_fd = 0;
         if (next_table) {
             n_fd = min(kFastDraws, 2 * (n - w.emitted) + 256);
-            if (tid == 0) s_fast = 1;
-            __syncthreads();
-            for (int i = tid; i < n_fd; i += kWalkThreads) {
-                const uint64_t v = stream_u64(cfg.key_slide, w.c_slide + 1 + (uint64_t)i);
-                int sidx;
-                if (cfg.strategy == 0) {
-                    const uint64_t nn = (uint64_t)cfg.n_slides;
-                    sidx = randrange_accepts(v, randrange_limit(nn)) ? (int)(v % nn) : -1;
-                } else {
-                    const double u = __dadd_rn(0.0, __dmul_rn(u64_to_unit(v), __dsub_rn(k_total_weight(cfg, slides), 0.0)));
-                    double acc = 0.0;
-                    sidx = cfg.n_slides - 1;
-                    for (int k = 0; k < cfg.n_slides; ++k) {
-                        acc = __dadd_rn(acc, slides[k].weight);
-                        if (u < acc) {
-                            sidx = k;
-                            break;
-                        }
-                    }
-                }
-                if (sidx < 0) s_fast = 0;  // a rejected draw (p ~ n / 2^64): the general walk handles it
-                fdraw[i] = sidx;
+            // na is 4-byte aligned in shared memory (window % 32 == 0); 16-byte global reads
+            const int na_words = cfg.n_slides * window / 2;
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(ws.na);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(na);
+            for (int i = tid; i < na_words / 4; i += kWalkThreads) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + i);
+                dst[4 * i] = v.x;
+                dst[4 * i + 1] = v.y;
+                dst[4 * i + 2] = v.z;
+                dst[4 * i + 3] = v.w;
             }
+            for (int i = (na_words / 4) * 4 + tid; i < na_words; i += kWalkThreads) dst[i] = __ldg(src + i);
+            for (int i = tid; i < n_fd; i += kWalkThreads) fdraw[i] = __ldg(ws.fdraw + i);
+            if (tid == 0) s_fast = *ws.draws_ok == kCountBase;
             __syncthreads();
         }
+        PF_WT(2);
         PF_WT(3);
         if (next_table && s_fast) {
             if (tid == 0) {  // one thread: no divergence bookkeeping inside the chain
@@ -757,10 +882,8 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     sample_begin_kernel<<<1, 1, 0, st>>>(state_dev);
     int rc = after_launch("sample_begin_kernel");
     if (rc) return rc;
-    // small blocks: most candidates finish in the whole-window shortcut, and a boundary window's
-    // warp must not pin idle warps' shared memory (measured: 8-warp blocks ran at 15 % occupancy)
-    const int warps = 2;
-    // chunked row masks (1.3 KB per warp at grid 128): an eval block fits beside a multi-crop CTA
+    const int warps = kEvalWarps;
+    // per warp: slab/edge cache + chunked row masks (3.7 KB at grid 128)
     const size_t eval_smem = (size_t)warps * overlap_smem_bytes_chunked(cfg->grid);
     const size_t bm_bytes_all = (size_t)cfg->n_slides * (window / 32) * 4;
     const int bm_in_smem = rounds > 0 && bm_bytes_all <= 160 * 1024;
@@ -776,6 +899,21 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     rc = check_cuda(cudaFuncSetAttribute(sample_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)eval_smem), "cudaFuncSetAttribute");
     if (rc) return rc;
+    static thread_local int eval_grid = 0, eval_grid_dev = -1;  // resident evaluation blocks, whole GPU
+    static thread_local size_t eval_grid_smem = 0;
+    int cur_dev = 0;
+    if ((rc = check_cuda(cudaGetDevice(&cur_dev), "cudaGetDevice"))) return rc;
+    if (eval_grid == 0 || eval_grid_dev != cur_dev || eval_grid_smem != eval_smem) {
+        int dev = cur_dev, sms = 0, per_sm = 0;
+        if ((rc = check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute")))
+            return rc;
+        if ((rc = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_eval_kernel, warps * 32,
+                                                                           eval_smem), "cudaOccupancy")))
+            return rc;
+        eval_grid = std::max(1, sms * std::max(1, per_sm));
+        eval_grid_dev = cur_dev;
+        eval_grid_smem = eval_smem;
+    }
     SamplerWs ws{};
     if (rounds > 0) ws = carve_ws(workspace, cfg->n_slides, window);
     EvalConsts consts{};
@@ -785,13 +923,23 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
         const size_t bm_bytes = (size_t)cfg->n_slides * (window / 32) * 4;
         rc = check_cuda(cudaMemsetAsync(ws.bitmaps, 0, bm_bytes, st), "cudaMemsetAsync");
         if (rc) return rc;
-        rc = check_cuda(cudaMemsetAsync(ws.reject_at, 0x7f, 4, st), "cudaMemsetAsync");
+        // reject_at, n_queue and draws_ok all start at kCountBase (0x7f bytes)
+        rc = check_cuda(cudaMemsetAsync(ws.reject_at, 0x7f, 12, st), "cudaMemsetAsync");
         if (rc) return rc;
         const int64_t cands = (int64_t)cfg->n_slides * window;
-        const int64_t blocks = (cands + warps - 1) / warps;
+        sample_classify_kernel<<<(unsigned)((cands + 255) / 256), 256, 0, st>>>(*cfg, slides_dev, state_dev, ws, window,
+                                                                                n, consts);
+        if ((rc = after_launch("sample_classify_kernel"))) return rc;
+        const int64_t blocks = std::min<int64_t>((cands + warps - 1) / warps, eval_grid);
         sample_eval_kernel<<<(unsigned)blocks, warps * 32, eval_smem, st>>>(*cfg, slides_dev, state_dev, ws, window, n,
                                                                              consts);
         if ((rc = after_launch("sample_eval_kernel"))) return rc;
+        if (next_table) {
+            const int draw_blocks = (std::min(kFastDraws, 2 * n + 256) + kTableThreads - 1) / kTableThreads;
+            sample_table_kernel<<<cfg->n_slides + draw_blocks, kTableThreads, 0, st>>>(*cfg, slides_dev, state_dev, ws,
+                                                                                      window, n);
+            if ((rc = after_launch("sample_table_kernel"))) return rc;
+        }
         sample_walk_kernel<<<1, kWalkThreads, walk_smem, st>>>(*cfg, slides_dev, slide_descs_dev, state_dev, ws,
                                                                 window, n, 1, r == rounds - 1, bm_in_smem,
                                                                 next_table, ws.emits, out_dev);

@@ -129,6 +129,29 @@ class ForegroundPolygon:
             self._blob = torch.from_numpy(self.index_blob()).cuda()
         return self._blob
 
+    def device_raster(self, cell: float | None = None):
+        """Classification raster of the polygon in HBM (pf_polygon_raster_build, cached): 2-bit
+        cells of ``cell`` px (default: 32, doubled until the raster has at most 16 M cells)."""
+        torch = N.require_cuda()
+        bbox = (C.c_double * 4)(*self.bounding_box())
+        if cell is None:
+            cell = 32.0
+            while ((bbox[2] - bbox[0]) / cell + 3) * ((bbox[3] - bbox[1]) / cell + 3) > (1 << 24):
+                cell *= 2.0
+        key = float(cell)
+        cache = getattr(self, "_rasters", None)
+        if cache is None:
+            cache = self._rasters = {}
+        if key not in cache:
+            nbytes = C.c_int64(0)
+            N.check(N.lib().pf_polygon_raster_bytes(bbox, key, C.byref(nbytes)), "pf_polygon_raster_bytes")
+            out = torch.empty((nbytes.value,), dtype=torch.uint8, device="cuda")
+            st = torch.cuda.current_stream()
+            N.check(N.lib().pf_polygon_raster_build(self.device_blob().data_ptr(), bbox, key, out.data_ptr(),
+                                                    nbytes.value, N.stream_ptr(st)), "pf_polygon_raster_build")
+            cache[key] = out
+        return cache[key]
+
 
 def _to_device_rgb(thumbnail):
     torch = N.require_cuda()

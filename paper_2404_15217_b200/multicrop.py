@@ -161,7 +161,7 @@ class MultiCropLoader:
     """
 
     def __init__(self, slides, sampler_config, mc_config: MultiCropConfig | None = None, *, batch_size: int = 1024,
-                 rank: int = 0, dtype: str = "bf16", mean=IMAGENET_MEAN, std=IMAGENET_STD, window=None, rounds: int = 2,
+                 rank: int = 0, dtype: str = "bf16", mean=IMAGENET_MEAN, std=IMAGENET_STD, window=None, rounds: int = 1,
                  prefetch: bool = True, cap: int | None = None, aug_seed: int | None = None):
         torch = N.require_cuda()
         from .sampler import CappedSampler, GpuSampler
@@ -242,6 +242,10 @@ class MultiCropLoader:
                 self._ready[cur] = torch.cuda.Event()
                 self._ready[cur].record(self._side)
             st.wait_event(self._ready[cur])
+            if self.tiers is not None and self.tiers.stale():
+                # a tier pool was resized after this batch was prefetched: make its tiles resident
+                # in the new pool
+                self.tiers.prefetch(self.specs_slots[cur], n, stream=st)
             mark("sample_wait")
         specs = self.specs_slots[cur]
         # the crop parameters (and the resample) are launched before the next step's sampler so
@@ -291,7 +295,7 @@ class MultiCropLoader:
 
     def kernels_per_batch(self) -> int:
         """CUDA kernels one next_batch launches (sampler rounds + resample + params + 2 multi-crop groups)."""
-        smp = 1 + (2 * self.sampler.rounds if self.sampler.all_fit and self.sampler.rounds > 0 else 1)
+        smp = 1 + (4 * self.sampler.rounds if self.sampler.all_fit and self.sampler.rounds > 0 else 1)
         return smp + (1 if self.needs_resample else 0) + 1 + (self.mc.n_global > 0) + (self.mc.n_local > 0)
 
 

@@ -214,7 +214,7 @@ class RegionLoader:
     """
 
     def __init__(self, slides, sampler_config, *, batch_size: int = 256, dtype: str = "f32", layout: str = "nchw",
-                 mean=IMAGENET_MEAN, std=IMAGENET_STD, prefetch: bool = True, window=None, rounds: int = 2,
+                 mean=IMAGENET_MEAN, std=IMAGENET_STD, prefetch: bool = True, window=None, rounds: int = 1,
                  chunk: int | None = None):
         torch = N.require_cuda()
         from .sampler import GpuSampler

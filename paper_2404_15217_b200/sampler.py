@@ -193,7 +193,7 @@ class GpuSampler:
     """
 
     def __init__(self, config: SamplerConfig, slides, *, slide_set=None, window: int | None = None,
-                 rounds: int = 4, grid: int = OVERLAP_GRID):
+                 rounds: int = 4, grid: int = OVERLAP_GRID, raster: bool = True):
         torch = N.require_cuda()
         if not slides:
             raise NoSamplableSlideError("no slides provided")
@@ -241,6 +241,10 @@ class GpuSampler:
             blob = poly.device_blob()
             blobs.append(blob)
             t.poly_blob = int(blob.data_ptr())
+            if raster:  # classification raster: windows far from every edge skip the lattice test
+                ras = poly.device_raster()
+                blobs.append(ras)
+                t.raster = int(ras.data_ptr())
             bx0, by0, bx1, by1 = poly.bounding_box()
             t.bbox[:] = [bx0, by0, bx1, by1]
             t.weight = ws[i]
@@ -280,14 +284,19 @@ class GpuSampler:
         self._ws = None
         self._ws_stream = None
         self._ws_window = 0
+        self._stats_host = torch.empty(C.sizeof(N.SamplerState), dtype=torch.uint8, pin_memory=True)
+        self._stats_event = None
 
     def _window_for(self, n: int) -> int:
         if self.window:
             return max(32, (self.window + 31) // 32 * 32)
-        # attempts for n accepts ~ negative binomial: mean n/p, sd sqrt(n(1-p))/p; 3 sd of slack,
-        # further rounds cover the rare overflow (every offset is evaluated for every slide)
+        # attempts for n accepts ~ negative binomial: mean n/p, sd sqrt(n(1-p))/p; 4 sd of slack
+        # (overflow ~3e-5 per call), further rounds or the walk's exact path cover the rest.  p is
+        # the stream's observed acceptance rate once a previous call's counters are back on the
+        # host (copied asynchronously, never waited for), the polygon-area estimate before.
+        self._poll_stats()
         p = self.p_est
-        w = int(n / p + 3.0 * math.sqrt(n * (1.0 - p)) / p) + 32
+        w = int(n / p + 4.0 * math.sqrt(n * (1.0 - p)) / p) + 32
         return min(max(32, (w + 31) // 32 * 32), 1 << 16)
 
     def next_batch(self, n: int, out=None, stream=None):
@@ -314,7 +323,20 @@ class GpuSampler:
                               self.rounds, 1 if self.all_fit else 0, N.stream_ptr(stream)),
             "pf_sample",
         )
+        if self._stats_event is None:  # the counters ride back to the host for the next window
+            with torch.cuda.stream(st):
+                self._stats_host.copy_(self.state[:C.sizeof(N.SamplerState)], non_blocking=True)
+            self._stats_event = torch.cuda.Event()
+            self._stats_event.record(st)
         return out
+
+    def _poll_stats(self) -> None:
+        if self._stats_event is None or not self._stats_event.query():
+            return
+        st = N.SamplerState.from_buffer_copy(self._stats_host.numpy().tobytes())
+        self._stats_event = None
+        if st.attempts >= 256 and st.seq > 0:
+            self.p_est = max(0.02, min(1.0, st.seq / st.attempts))
 
     def state_host(self) -> N.SamplerState:
         return N.SamplerState.from_buffer_copy(self.state.cpu().numpy().tobytes())

@@ -143,11 +143,11 @@ def resize_pool(slide, n_slots: int, chunk: int = 2048) -> None:
     tile_map[idx[:n_slots]] = np.arange(1, n_slots + 1, dtype=np.int32)
     owner = np.full(n_slots + 1, -1, dtype=np.int32)
     owner[1:] = idx[:n_slots].astype(np.int32)
-    new = TileTierState(st.store, st.host_index.cpu().numpy(), owner, ny * nx, n_slots, level, st.max_miss)
-    new.tile_ids = idx
+    # in place: TierSets built earlier hold this state object and rebuild their device records
+    # when its version changes
+    st.reset_pool(owner, ny * nx, n_slots)
     slide.levels[level] = slots.view(n_slots + 1, T, T, 3)
     slide.tile_maps[level] = torch.from_numpy(tile_map).cuda()
-    slide.tier = new
     slide.desc = slide._make_desc()
     slide._own_set = None
     for ss in list(slide._sets):
@@ -162,14 +162,24 @@ class TileTierState:
 
         self.store = store
         self.host_index = torch.from_numpy(host_index).cuda()
-        self.owner = torch.from_numpy(owner).cuda()
-        self.last_use = torch.zeros(n_slots + 1, dtype=torch.int32, device="cuda")
-        self.requested = torch.zeros(n_tiles, dtype=torch.int32, device="cuda")
+        self.level, self.max_miss = level, max_miss
         self.miss_list = torch.zeros(max_miss, dtype=torch.int32, device="cuda")
         self.victims = torch.zeros(max_miss, dtype=torch.int32, device="cuda")
         self.counters = torch.zeros(8, dtype=torch.int32, device="cuda")
-        self.level, self.n_slots, self.max_miss = level, n_slots, max_miss
         self.batch = 1  # last batch id issued against this level (ids only grow, whoever prefetches)
+        self.version = 0
+        self.reset_pool(owner, n_tiles, n_slots)
+
+    def reset_pool(self, owner, n_tiles: int, n_slots: int) -> None:
+        """New slot pool bookkeeping (slot contents and the tile map are the caller's)."""
+        import torch
+
+        self.owner = torch.from_numpy(np.ascontiguousarray(owner, dtype=np.int32)).cuda()
+        self.last_use = torch.zeros(n_slots + 1, dtype=torch.int32, device="cuda")
+        self.requested = torch.zeros(n_tiles, dtype=torch.int32, device="cuda")
+        self.counters[2] = 0  # clock hand
+        self.n_slots = n_slots
+        self.version += 1
 
     def record(self) -> TileTier:
         t = TileTier()
@@ -196,19 +206,33 @@ class TierSet:
 
         self.slide_set = slide_set
         self.states = [getattr(s, "tier", None) for s in slide_set.slides]
+        self._versions = None
+        self.dev = None
+        self._upload()
+        self.max_fill = max([s.max_miss for s in self.states if s is not None] or [1])
+
+    def _upload(self) -> None:
+        import torch
+
         recs = (TileTier * len(self.states))()
         for i, stt in enumerate(self.states):
             if stt is not None:
                 recs[i] = stt.record()
         self.dev = torch.frombuffer(bytearray(bytes(recs)), dtype=torch.uint8).cuda()
-        self.max_fill = max([s.max_miss for s in self.states if s is not None] or [1])
+        self._versions = [s.version if s is not None else -1 for s in self.states]
 
     @property
     def active(self) -> bool:
         return any(s is not None for s in self.states)
 
+    def stale(self) -> bool:
+        """A pool was resized since the last prefetch (its device records moved)."""
+        return [s.version if s is not None else -1 for s in self.states] != self._versions
+
     def prefetch(self, specs_dev, n: int, stream=None, max_window: int = 512) -> int:
         """Make the tiles of these (planned) specs resident for the next batch; returns the batch id."""
+        if self.stale():
+            self._upload()  # a pool was resized since: device records point at the new arrays
         live = [s for s in self.states if s is not None]
         batch = 1 + max(s.batch for s in live)
         for s in live:

@@ -37,7 +37,7 @@ def test_library_exports_header(native):
     exported = set(re.findall(r" T (pf_\w+)", out))
     assert set(syms) <= exported, set(syms) - exported
     assert set(syms) == set(native.exported_symbols()), "python binding must cover the header exactly"
-    assert native.lib().pf_abi_version() == 2
+    assert native.lib().pf_abi_version() == 3
 
 
 def test_errors_without_device(native):

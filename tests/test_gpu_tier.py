@@ -76,3 +76,21 @@ def test_pool_smaller_than_a_batch_faults(pf, cuda):
     ld.next_batch()
     with pytest.raises(pf.errors.CapacityError):
         ld.check()
+
+
+def test_resize_pool_under_a_live_loader(pf, cuda):
+    """resize_pool after a loader was built: the loader's tier records follow the new pool."""
+    torch = cuda
+    d, _, poly = _slide_and_poly(pf, 14)
+    t, poly_t, st, n0 = _tiered(pf, 14, 0.3)
+    cfg = pf.SamplerConfig(patch_size=224, seed=5, target_mpps=[(0.25, 1.0), (0.5, 1.0)])
+    a = pf.mc.MultiCropLoader([(d, poly)], cfg, batch_size=32, dtype="u8")
+    b = pf.mc.MultiCropLoader([(t, poly_t)], cfg, batch_size=32, dtype="u8")
+    for step in range(8):
+        if step == 3:
+            pf.TR.resize_pool(t, int(0.5 * n0))
+            assert st.n_slots == int(0.5 * n0)
+        oa, ob = a.next_batch(), b.next_batch()
+        torch.cuda.synchronize()
+        b.check()
+        assert torch.equal(oa["global_crops"], ob["global_crops"]) and torch.equal(oa["local_crops"], ob["local_crops"])

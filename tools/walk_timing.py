@@ -10,7 +10,7 @@ smp = pf.GpuSampler(pf.SamplerConfig(patch_size=224, seed=plan.sampler_seed), sl
 for it in range(4):
     smp.next_batch(1024)
     torch.cuda.synchronize()
-    for r, off in (("round 1", 8), ("round 2", 72)):
+    for r, off in (("round 1", 32), ("round 2", 96)):
         t = smp._ws[off:off + 6 * 8].cpu().numpy().view(np.uint64).astype(np.int64)
         print(r, "phases (us): start->bitmaps %.1f, ->tables %.1f, ->draws %.1f, ->walk %.1f, ->materialise %.1f"
               % tuple((t[1:] - t[:-1]) / 1000.0))
