@@ -288,8 +288,9 @@ int pf_polygon_index_build(const double* xy, const int64_t* ring_off, int32_t n_
 
 /* Coarse classification raster of a polygon for the sampler's acceptance test
  * (no reference counterpart: a precomputed filter in front of overlap_fraction,
- * pkg/foreground.py:246-286).  Square cells of `cell` px (a power of two >= 8)
- * covering the bounding box plus one cell; each cell is 2 bits: 01 every point
+ * pkg/foreground.py:246-286).  Two levels of square cells, `cell` px (a power of
+ * two, 8..16384) and 4 `cell` px, each covering the bounding box plus one cell;
+ * each cell is 2 bits: 01 every point
  * of the cell (closed, grown by 1 px) is inside, 00 every point outside, 1x an
  * edge comes within 1 px of it.  A window whose cells are all 01 (all 00) has
  * overlap_fraction 1.0 (0.0) exactly, since the even-odd parity is constant over

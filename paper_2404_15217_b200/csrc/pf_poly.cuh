@@ -504,6 +504,12 @@ __device__ inline int raster_decide_thread(const RasterHeader* R, double x, doub
 // within rounding of a raster cell border, and the 1 px growth of a clean cell covers it.
 __device__ inline void raster_bounds_thread(const RasterHeader* R, double x, double y, double w, int grid, int& lo,
                                             int& hi) {
+    {  // a window 16 or more cells wide takes the coarse level (the common path reads <= 16 columns)
+        const double ic0 = __ldg(&R->inv_cell), ox0 = __ldg(&R->ox);
+        const int64_t coarse = __ldg(&R->coarse);
+        if (coarse && (int)floor((x + w - ox0) * ic0) - (int)floor((x - ox0) * ic0) >= 16)
+            R = reinterpret_cast<const RasterHeader*>(reinterpret_cast<const uint8_t*>(R) + coarse);
+    }
     const double ox = __ldg(&R->ox), oy = __ldg(&R->oy), C = __ldg(&R->cell), ic = __ldg(&R->inv_cell);
     const int nx = __ldg(&R->nx), ny = __ldg(&R->ny), pitch = __ldg(&R->pitch);
     const uint32_t* words = reinterpret_cast<const uint32_t*>(R + 1);

@@ -28,8 +28,10 @@ constexpr int32_t kPolyMagic = 0x50464231;  // "PFB1"
 struct RasterHeader {
     double ox, oy, cell, inv_cell;  // cell (i, j) covers [ox + i*cell, ox + (i+1)*cell) x ...
     int32_t nx, ny, pitch, magic;
-    int64_t _reserved[2];
+    int64_t coarse;                 // byte offset of the next (4x coarser) level's header, or 0
+    int64_t _reserved;
 };
+constexpr int kRasterLevels = 2;   // cell and 4 * cell: windows up to ~15 cells wide at either
 constexpr int32_t kRasterMagic = 0x50465231;  // "PFR1"
 constexpr uint32_t kRasterInside = 0x55555555u;
 

@@ -2,7 +2,8 @@
 // a precomputed filter in front of the sampler's overlap test (pkg/foreground.py:246-286,
 // called from sample_patch, pkg/sampler.py:174-179).
 //
-// Cells of `cell` px cover the polygon's bounding box plus one cell on every side.  A cell is
+// Two levels, cells of `cell` and 4 `cell` px (wide windows read the coarse one), each covering
+// the polygon's bounding box plus one cell on every side.  A cell is
 // "dirty" when some edge comes within 1 px of it; otherwise no edge meets the cell grown by
 // 1 px, the even-odd parity is the same at every point of that grown cell, and the cell's
 // centre (traced with the device even-odd test) gives it.  The sampler's evaluation warps
@@ -98,38 +99,55 @@ bool raster_geometry(const double* bbox, double cell, RasterHeader* h) {
     return true;
 }
 
+// Levels: cell, 4 cell, ... (kRasterLevels), each header followed by its words, 16-byte aligned.
+bool raster_levels(const double* bbox, double cell, RasterHeader (&hs)[kRasterLevels], int64_t (&offs)[kRasterLevels],
+                   int64_t* total) {
+    int64_t at = 0;
+    for (int l = 0; l < kRasterLevels; ++l) {
+        if (!raster_geometry(bbox, cell * (double)(1 << (2 * l)), &hs[l])) return false;
+        offs[l] = at;
+        at += (int64_t)sizeof(RasterHeader) + ((int64_t)hs[l].ny * hs[l].pitch * 4 + 15) / 16 * 16;
+    }
+    for (int l = 0; l + 1 < kRasterLevels; ++l) hs[l].coarse = offs[l + 1] - offs[l];
+    *total = at;
+    return true;
+}
+
 }  // namespace
 }  // namespace pf
 
 using namespace pf;
 
 extern "C" int pf_polygon_raster_bytes(const double* bbox, double cell, int64_t* bytes) {
-    RasterHeader h;
-    if (!bytes || !raster_geometry(bbox, cell, &h))
-        return fail(PF_ERR_INVALID_ARG, "pf_polygon_raster_bytes: bad bbox or cell (power of two, 8..65536)");
-    *bytes = (int64_t)sizeof(RasterHeader) + (int64_t)h.ny * h.pitch * 4;
+    RasterHeader hs[kRasterLevels];
+    int64_t offs[kRasterLevels];
+    if (!bytes || !raster_levels(bbox, cell, hs, offs, bytes))
+        return fail(PF_ERR_INVALID_ARG, "pf_polygon_raster_bytes: bad bbox or cell (power of two, 8..16384)");
     return PF_OK;
 }
 
 extern "C" int pf_polygon_raster_build(const void* poly_blob_dev, const double* bbox, double cell, void* raster_dev,
                                        int64_t raster_bytes, void* stream) {
-    RasterHeader h;
-    if (!poly_blob_dev || !raster_dev || !raster_geometry(bbox, cell, &h))
+    RasterHeader hs[kRasterLevels];
+    int64_t offs[kRasterLevels], need = 0;
+    if (!poly_blob_dev || !raster_dev || !raster_levels(bbox, cell, hs, offs, &need))
         return fail(PF_ERR_INVALID_ARG, "pf_polygon_raster_build: bad arguments");
-    const int64_t need = (int64_t)sizeof(RasterHeader) + (int64_t)h.ny * h.pitch * 4;
     if (raster_bytes < need) return fail(PF_ERR_INVALID_ARG, "pf_polygon_raster_build: raster buffer too small");
     cudaStream_t st = as_stream(stream);
-    uint8_t* out = reinterpret_cast<uint8_t*>(raster_dev);
-    uint32_t* words = reinterpret_cast<uint32_t*>(out + sizeof(RasterHeader));
-    int rc = check_cuda(cudaMemcpyAsync(out, &h, sizeof(h), cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
-    if (rc) return rc;
-    rc = check_cuda(cudaMemsetAsync(words, 0, (size_t)h.ny * h.pitch * 4, st), "cudaMemsetAsync");
-    if (rc) return rc;
-    raster_mark_kernel<<<592, 256, 0, st>>>(poly_blob_dev, h, words);
-    if ((rc = after_launch("raster_mark_kernel"))) return rc;
-    const int threads = ((h.nx + 255) / 256) * h.ny;
-    raster_classify_kernel<<<(threads + 127) / 128, 128, 0, st>>>(poly_blob_dev, h, words);
-    if ((rc = after_launch("raster_classify_kernel"))) return rc;
-    // the header is copied from this stack frame: finish before returning
+    int rc = PF_OK;
+    for (int l = 0; l < kRasterLevels; ++l) {
+        const RasterHeader& h = hs[l];
+        uint8_t* out = reinterpret_cast<uint8_t*>(raster_dev) + offs[l];
+        uint32_t* words = reinterpret_cast<uint32_t*>(out + sizeof(RasterHeader));
+        if ((rc = check_cuda(cudaMemcpyAsync(out, &h, sizeof(h), cudaMemcpyHostToDevice, st), "cudaMemcpyAsync")))
+            return rc;
+        if ((rc = check_cuda(cudaMemsetAsync(words, 0, (size_t)h.ny * h.pitch * 4, st), "cudaMemsetAsync"))) return rc;
+        raster_mark_kernel<<<592, 256, 0, st>>>(poly_blob_dev, h, words);
+        if ((rc = after_launch("raster_mark_kernel"))) return rc;
+        const int threads = ((h.nx + 255) / 256) * h.ny;
+        raster_classify_kernel<<<(threads + 127) / 128, 128, 0, st>>>(poly_blob_dev, h, words);
+        if ((rc = after_launch("raster_classify_kernel"))) return rc;
+    }
+    // the headers are copied from this stack frame: finish before returning
     return check_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
 }

@@ -26,12 +26,14 @@ def polys(cuda):
     return pf, out
 
 
-def _decode(raster):
+def _decode(raster, level=0):
     raw = raster.cpu().numpy()
+    for _ in range(level):  # header.coarse: byte offset of the next level
+        raw = raw[int(raw[48:56].view(np.int64)[0]):]
     ox, oy, cell, inv = raw[:32].view(np.float64)
     nx, ny, pitch, magic = raw[32:48].view(np.int32)
     assert magic == 0x50465231
-    words = raw[64:].view(np.uint32).reshape(ny, pitch)
+    words = raw[64:64 + 4 * ny * pitch].view(np.uint32).reshape(ny, pitch)
     codes = np.zeros((ny, pitch * 16), dtype=np.uint8)
     for k in range(16):
         codes[:, k::16] = (words >> (2 * k)) & 3
@@ -49,11 +51,12 @@ def _fractions(pf, poly, rects, grid=32):
     return out.cpu().numpy()
 
 
-def test_clean_cells_have_one_parity(polys):
+@pytest.mark.parametrize("level", [0, 1])
+def test_clean_cells_have_one_parity(polys, level):
     pf, ps = polys
-    rs = np.random.default_rng(0)
+    rs = np.random.default_rng(level)
     for poly in ps:
-        ox, oy, cell, codes = _decode(poly.device_raster())
+        ox, oy, cell, codes = _decode(poly.device_raster(), level)
         ny, nx = codes.shape
         clean = np.argwhere(codes < 2)
         assert len(clean) > 0.5 * codes.size and (codes == 1).sum() > 0 and (codes == 2).sum() > 0
@@ -120,7 +123,7 @@ def _bounds(ox, oy, cell, codes, x, y, w, grid):
     ny, nx = codes.shape
     inv = grid / w
 
-    def span(origin, p0, c):
+    def span(origin, p0, c):  # noqa: E306
         c0 = origin + c * cell
         k0 = max(0, int(np.ceil((c0 - p0) * inv)))
         k1 = min(grid - 1, int(np.floor((c0 + cell - p0) * inv)) - 1)
@@ -143,19 +146,27 @@ def _bounds(ox, oy, cell, codes, x, y, w, grid):
 
 def test_count_bounds_hold(polys):
     """The classification pass's covered-cell bounds bracket overlap_fraction's exact count, and
-    are tight enough to settle most boundary windows at the sampler's threshold."""
+    are tight enough to settle most boundary windows at the sampler's threshold (windows 16 or
+    more fine cells wide read the coarse level, as raster_bounds_thread does)."""
     pf, ps = polys
     rs = np.random.default_rng(2)
     grid = 128
     need = 0.4 * grid * grid
     for poly in ps:
-        ox, oy, cell, codes = _decode(poly.device_raster())
+        levels = [_decode(poly.device_raster(), lv) for lv in (0, 1)]
         bx0, by0, bx1, by1 = poly.bounding_box()
         n = 3000
-        w = rs.choice([224.0, 448.0], size=n)
+        w = rs.choice([224.0, 448.0, 896.0, 1792.0], size=n)
         x = np.floor(bx0 + rs.random(n) * (bx1 - bx0))
         y = np.floor(by0 + rs.random(n) * (by1 - by0))
-        b = np.array([_bounds(ox, oy, cell, codes, x[i], y[i], w[i], grid) for i in range(n)])
+
+        def bounds(i):
+            ox, oy, cell, codes = levels[0]
+            if int(np.floor((x[i] + w[i] - ox) / cell)) - int(np.floor((x[i] - ox) / cell)) >= 16:
+                ox, oy, cell, codes = levels[1]
+            return _bounds(ox, oy, cell, codes, x[i], y[i], w[i], grid)
+
+        b = np.array([bounds(i) for i in range(n)])
         count = np.rint(_fractions(pf, poly, np.stack([x, y, w, w], axis=1), grid=grid) * grid * grid)
         assert np.all(b[:, 0] <= count) and np.all(count <= b[:, 1])
         boundary = (count > 0) & (count < grid * grid)
