@@ -386,10 +386,13 @@ def timed_run(feed, args, torch, dist, world, local, N):
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.nvtx.range_push("timed")
     start.record(stream)
+    res_ev = []
     for _ in range(args.steps):
         marks = []
-        loader.next_batch(marks=marks)
+        out = loader.next_batch(marks=marks)
         marks_all.append(marks)
+        if isinstance(out, dict) and out.get("resample_events") is not None:
+            res_ev.append(out["resample_events"])
     end.record(stream)
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
@@ -409,6 +412,8 @@ def timed_run(feed, args, torch, dist, world, local, N):
         for (_, ea), (b, eb) in zip(marks[:-1], marks[1:]):
             stages.setdefault(b, []).append(ea.elapsed_time(eb))
     stage_ms = {k: sum(v) / len(v) for k, v in stages.items()}
+    if res_ev:  # the resample runs on the loader's side stream (overlapping the previous multi-crop)
+        stage_ms["resample"] = sum(a.elapsed_time(b) for a, b in res_ev) / len(res_ev)
     return float(t.item()), stage_ms, launches, clk.summary()
 
 

@@ -356,16 +356,23 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
         for (int i = 0; i < 9; ++i) r[i] = wp[i];
 #pragma unroll
         for (int i = 0; i < 8; ++i) A[i] = __funnelshift_r(r[i], r[i + 1], sh);
+        // outputs k and k + 2 of a channel in the two 16-bit lanes of one word: tap t of output k
+        // is byte 6k + c + 3t of A, and of output k + 2 the byte 12 further, i.e. the same byte of
+        // the word three on -- one byte_perm per tap pair
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            uint32_t pb[10];  // channel c of the 10 pixels: byte 3i + c
+            uint32_t pair[2];
 #pragma unroll
-            for (int i = 0; i < 10; ++i) pb[i] = (A[(3 * i + c) >> 2] >> (8 * ((3 * i + c) & 3))) & 0xffu;
-            uint32_t o = 0;
+            for (int k = 0; k < 2; ++k) {
+                uint32_t tap[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                o |= ((pb[2 * k] + pb[2 * k + 3] + 3u * (pb[2 * k + 1] + pb[2 * k + 2]) + 4u) >> 3) << (8 * k);
-            outw[c] = o;
+                for (int t = 0; t < 4; ++t) {
+                    const int b = 6 * k + c + 3 * t, i = b >> 2, o = b & 3;
+                    tap[t] = __byte_perm(A[i], A[i + 3], (uint32_t)(o | ((o + 4) << 8))) & 0x00ff00ffu;
+                }
+                pair[k] = ((tap[0] + tap[3] + 3u * (tap[1] + tap[2]) + 0x00040004u) >> 3) & 0x00ff00ffu;
+            }
+            outw[c] = __byte_perm(pair[0], pair[1], 0x6240u);  // bytes k = 0, 1, 2, 3
         }
         store3(rr, x0, outw);
     }

@@ -154,6 +154,9 @@ def multicrop(slide_set, specs_dev, params_dev, cfg: MultiCropConfig, *, dtype: 
 class MultiCropLoader:
     """Online patching training feed: sampler -> (resample) -> params -> fused multi-crop.
 
+    The sampler (and the resample of mixed-mpp sources) of step k+1 runs on a side stream
+    while step k's multi-crop runs.
+
     ``slides``: list of (GpuSlide, ForegroundPolygon).  Each ``next_batch``
     enqueues the whole step on the current stream and returns device tensors;
     per-rank streams follow the reference's seed + rank sharding for the
@@ -194,7 +197,12 @@ class MultiCropLoader:
         self._free = [torch.cuda.Event(), torch.cuda.Event()]
         self._next_slot = 0
         self.params = torch.empty((batch_size, self.mc.n_crops, 64), dtype=torch.uint8, device="cuda")
-        self.src = torch.empty((batch_size, S, S, 3), dtype=torch.uint8, device="cuda") if self.needs_resample else None
+        # resampled sources, one per slot: the next step's PIL resample runs on the side stream
+        # right after its sampler, under this step's multi-crop (memory-bound beside issue-bound)
+        self.src_slots = ([torch.empty((batch_size, S, S, 3), dtype=torch.uint8, device="cuda") for _ in range(2)]
+                          if self.needs_resample else [None, None])
+        self.src = self.src_slots[0]
+        self._res_ev = [None, None]  # (start, end) events of each slot's resample
         tdt = {"u8": torch.uint8, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
         self.out_global = torch.empty((self.mc.n_global, batch_size, 3, self.mc.global_size, self.mc.global_size),
                                       dtype=tdt, device="cuda")
@@ -208,9 +216,23 @@ class MultiCropLoader:
         self.tiers = ts if ts.active else None
 
     def _sample(self, slot: int, st) -> None:
+        """Specs of a slot, their tiles made resident (tiered slides) and, when some mpp needs it,
+        their resampled S x S sources -- all on stream ``st``."""
+        torch = N.require_cuda()
         self.specs_from.next_batch(self.batch_size, out=self.specs_slots[slot], stream=st)
         if self.tiers is not None:
             self.tiers.prefetch(self.specs_slots[slot], self.batch_size, stream=st)
+        if self.needs_resample:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            m = (C.c_float * 3)(0.5, 0.5, 0.5)
+            N.check(N.lib().pf_read_regions(self.slide_set.descs.data_ptr(), self.specs_slots[slot].data_ptr(),
+                                            self.batch_size, self.mc.src_size, N.PF_U8,
+                                            N.PF_HWC | N.PF_SKIP_PASSTHROUGH, C.cast(m, C.c_void_p),
+                                            C.cast(m, C.c_void_p), self.src_slots[slot].data_ptr(),
+                                            N.stream_ptr(st)), "pf_read_regions")
+            e1.record(st)
+            self._res_ev[slot] = (e0, e1)
 
     def next_batch(self, stream=None, marks: list | None = None) -> dict:
         """Enqueue one step and return its device tensors.
@@ -248,36 +270,27 @@ class MultiCropLoader:
                 self.tiers.prefetch(self.specs_slots[cur], n, stream=st)
             mark("sample_wait")
         specs = self.specs_slots[cur]
-        # the crop parameters (and the resample) are launched before the next step's sampler so
-        # that the sampler's speculative-evaluation blocks do not take the SMs first
+        src = self.src_slots[cur]
+        res_ev = self._res_ev[cur]
+        # the crop parameters are launched before the next step's sampler so that the sampler's
+        # speculative-evaluation blocks do not take the SMs first
         crop_params(self.mc, n, self.seed, self.rank, self.step, out=self.params, stream=st)
         mark("params")
-        if self.needs_resample:
-            m = (C.c_float * 3)(0.5, 0.5, 0.5)
-            N.check(N.lib().pf_read_regions(self.slide_set.descs.data_ptr(), specs.data_ptr(), n, self.mc.src_size,
-                                            N.PF_U8, N.PF_HWC | N.PF_SKIP_PASSTHROUGH, C.cast(m, C.c_void_p),
-                                            C.cast(m, C.c_void_p), self.src.data_ptr(), N.stream_ptr(st)),
-                    "pf_read_regions")
-            mark("resample")
         if self.prefetch:
             nxt = 1 - cur
             self._side.wait_event(self._free[nxt])  # step k-1 finished reading that slot
-            if self.needs_resample:  # the next sampler overlaps the multi-crop, not the resample
-                done = torch.cuda.Event()
-                done.record(st)
-                self._side.wait_event(done)
             self._sample(nxt, self._side)
             self._ready[nxt] = torch.cuda.Event()
             self._ready[nxt].record(self._side)
             self._next_slot = nxt
         multicrop(self.slide_set, specs, self.params, self.mc, dtype=self.dtype, mean=self.mean, std=self.std,
-                  src_hwc=self.src, out_global=self.out_global, out_local=self.out_local, stream=st)
+                  src_hwc=src, out_global=self.out_global, out_local=self.out_local, stream=st)
         mark("multicrop")
         if self.prefetch:
             self._free[cur].record(st)
         self.step += 1
         return {"global_crops": self.out_global, "local_crops": self.out_local, "specs": specs,
-                "params": self.params}
+                "params": self.params, "resample_events": res_ev}
 
     def check(self) -> None:
         """Synchronise and raise on a failed stream: NoSamplableSlideError from the sampler state,
