@@ -491,44 +491,62 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
     }
     if (use_table) {
         const uint32_t* bm_all = ws.bitmaps;
-        if (bitmaps_in_smem) {
-            for (int i = tid; i < cfg.n_slides * words; i += kWalkThreads) s_dyn[i] = ws.bitmaps[i];
-            bm_all = s_dyn;
-        }
-        __syncthreads();
-        PF_WT(1);
-        // next_table (sample_table_kernel, many CTAs): entry (slide, a) of the next-accept table
-        // and the call's slide draws, copied next to the bitmaps.  Layout after the bitmaps:
-        // [n_slides * words uint16 (unused)] na[n_slides][window] (uint16) fdraw[kFastDraws]
-        // semit[...]
-        uint16_t* nextw = reinterpret_cast<uint16_t*>(s_dyn + cfg.n_slides * words);
-        uint16_t* na = nextw + ((cfg.n_slides * words + 1) & ~1);
-        // int32 draws: 16-bit ones get packed in pairs by the compiler, which then waits on the
-        // prefetch load immediately
-        int32_t* fdraw = reinterpret_cast<int32_t*>(na + (((size_t)cfg.n_slides * window + 1) & ~(size_t)1));
-        // the fast walk's emits, (slide << 16) | window offset, in shared memory (a global store per
-        // draw on the one-thread chain costs more than the chain itself)
+        // Shared layout: bitmaps [n_slides * words] (padded to 16 B), next-accept table
+        // na[n_slides][window] (uint16), the call's slide draws fdraw[kFastDraws] (int32: 16-bit
+        // ones get packed in pairs by the compiler, which then waits on the prefetch load at
+        // once), the fast walk's emits semit[] ((slide << 16) | window offset: a global store
+        // per draw on the one-thread chain costs more than the chain itself)
+        const int bm_bytes = cfg.n_slides * words * 4;
+        uint16_t* na = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(s_dyn) + ((bm_bytes + 15) & ~15));
+        int32_t* fdraw = reinterpret_cast<int32_t*>(na + (size_t)cfg.n_slides * window);  // window % 32 == 0
         int32_t* semit = fdraw + kFastDraws;
         __shared__ int s_fast;
+        __shared__ __align__(8) uint64_t s_bar;
         int n_fd = 0;
         if (next_table) {
+            // bitmaps, table and draws in three bulk copies (TMA) on one mbarrier, issued by one
+            // thread: the per-thread copy loop of 98 KB was ~3 us of the walk
             n_fd = min(kFastDraws, 2 * (n - w.emitted) + 256);
-            // na is 4-byte aligned in shared memory (window % 32 == 0); 16-byte global reads
-            const int na_words = cfg.n_slides * window / 2;
-            const uint32_t* src = reinterpret_cast<const uint32_t*>(ws.na);
-            uint32_t* dst = reinterpret_cast<uint32_t*>(na);
-            for (int i = tid; i < na_words / 4; i += kWalkThreads) {
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + i);
-                dst[4 * i] = v.x;
-                dst[4 * i + 1] = v.y;
-                dst[4 * i + 2] = v.z;
-                dst[4 * i + 3] = v.w;
+            const uint32_t na_bytes = (uint32_t)cfg.n_slides * (uint32_t)window * 2u;
+            const uint32_t fd_bytes = ((uint32_t)n_fd * 4u + 15u) & ~15u;
+            const bool bm_bulk = (bm_bytes & 15) == 0;
+            const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+            if (tid == 0) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                const uint32_t total = na_bytes + fd_bytes + (bm_bulk ? (uint32_t)bm_bytes : 0u);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(total) : "memory");
+                auto bulk = [bar](void* dst, const void* src, uint32_t bytes) {
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            (uint32_t)__cvta_generic_to_shared(dst)),
+                        "l"(src), "r"(bytes), "r"(bar)
+                        : "memory");
+                };
+                if (bm_bulk) bulk(s_dyn, ws.bitmaps, (uint32_t)bm_bytes);
+                bulk(na, ws.na, na_bytes);
+                bulk(fdraw, ws.fdraw, fd_bytes);
+                s_fast = *ws.draws_ok == kCountBase;
             }
-            for (int i = (na_words / 4) * 4 + tid; i < na_words; i += kWalkThreads) dst[i] = __ldg(src + i);
-            for (int i = tid; i < n_fd; i += kWalkThreads) fdraw[i] = __ldg(ws.fdraw + i);
-            if (tid == 0) s_fast = *ws.draws_ok == kCountBase;
+            if (!bm_bulk)
+                for (int i = tid; i < cfg.n_slides * words; i += kWalkThreads) s_dyn[i] = ws.bitmaps[i];
+            __syncthreads();  // barrier initialised (and the fallback bitmap copy done)
+            uint32_t done = 0;
+            while (!done)
+                asm volatile(
+                    "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}"
+                    : "=r"(done)
+                    : "r"(bar)
+                    : "memory");
+            bm_all = s_dyn;
+        } else if (bitmaps_in_smem) {
+            for (int i = tid; i < cfg.n_slides * words; i += kWalkThreads) s_dyn[i] = ws.bitmaps[i];
+            bm_all = s_dyn;
+            __syncthreads();
+        } else {
             __syncthreads();
         }
+        PF_WT(1);
         PF_WT(2);
         PF_WT(3);
         if (next_table && s_fast) {
@@ -888,8 +906,8 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     const size_t bm_bytes_all = (size_t)cfg->n_slides * (window / 32) * 4;
     const int bm_in_smem = rounds > 0 && bm_bytes_all <= 160 * 1024;
     // next-accepted-offset table beside the bitmaps (uint16 offsets: window < 0xffff)
-    const size_t nt_bytes = bm_bytes_all + ((size_t)cfg->n_slides * (window / 32) + 1) / 2 * 4 +
-                            ((size_t)cfg->n_slides * window + 1) / 2 * 4 + (size_t)kFastDraws * 4 + (size_t)window * 4;
+    const size_t nt_bytes = (bm_bytes_all + 15) / 16 * 16 + (size_t)cfg->n_slides * window * 2 + (size_t)kFastDraws * 4 +
+                            (size_t)window * 4;
     const int next_table = bm_in_smem && window + cfg->max_attempts < 0x7fff && nt_bytes <= 200 * 1024;
     const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid),
                                       next_table ? nt_bytes : (bm_in_smem ? bm_bytes_all : (size_t)0));
