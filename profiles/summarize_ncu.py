@@ -17,7 +17,7 @@ HERE = Path(__file__).resolve().parent
 # one-off setup kernels (slide rendering, pyramid, thumbnail, mask, polygon index, RRC tables):
 # excluded so the shares are those of the timed step
 SETUP = ("synth_level0", "box_downsample", "box32_warp", "mask_kernel", "morph_kernel", "rrc_table_kernel",
-         "poly_index", "thumbnail", "field_kernel")
+         "poly_index", "thumbnail", "field_kernel", "raster_mark", "raster_classify")
 
 
 def launches(path):
