@@ -161,7 +161,9 @@ constexpr int kEvalWarps = 8;
 constexpr int32_t kCountBase = 0x7f7f7f7f;  // the round's memset value of reject_at / n_queue
 constexpr int kEvalParts = 4;  // a queued window's cell rows are counted by this many warps
 
-__global__ void __launch_bounds__(256) sample_classify_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
+constexpr int kClassifyThreads = 64;  // ~45 k candidates: small blocks spread evenly over the SMs
+
+__global__ void __launch_bounds__(kClassifyThreads) sample_classify_kernel(pf_sampler_config cfg, const pf_sampler_slide* slides,
                                                               const pf_sampler_state* state, SamplerWs ws, int window,
                                                               int n, EvalConsts k) {
     if (state->status != PF_OK || state->emitted >= n) return;
@@ -945,7 +947,8 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
         rc = check_cuda(cudaMemsetAsync(ws.reject_at, 0x7f, 12, st), "cudaMemsetAsync");
         if (rc) return rc;
         const int64_t cands = (int64_t)cfg->n_slides * window;
-        sample_classify_kernel<<<(unsigned)((cands + 255) / 256), 256, 0, st>>>(*cfg, slides_dev, state_dev, ws, window,
+        sample_classify_kernel<<<(unsigned)((cands + kClassifyThreads - 1) / kClassifyThreads), kClassifyThreads, 0,
+                                 st>>>(*cfg, slides_dev, state_dev, ws, window,
                                                                                 n, consts);
         if ((rc = after_launch("sample_classify_kernel"))) return rc;
         const int64_t blocks = std::min<int64_t>((cands + warps - 1) / warps, eval_grid);
