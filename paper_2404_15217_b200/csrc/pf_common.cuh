@@ -28,6 +28,13 @@
 
 namespace pf {
 
+// Dynamic shared memory of the launch (for PF_CHECK bounds on carved shared layouts).
+__device__ __forceinline__ uint32_t dynamic_smem_size() {
+    uint32_t r;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+
 // Thread-local last error; set by every failing entry point.
 void set_error(const std::string& msg);
 int fail(int status, const std::string& msg);

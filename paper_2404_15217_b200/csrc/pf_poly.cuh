@@ -224,6 +224,7 @@ __device__ inline void row_mask_cached(const PolyView& P, const SlabCache& c, in
     const int4 r = c.range[a];
     const int i_lo = centre ? r.z : r.x, i_hi = centre ? r.w : r.y;
     if (c.n_edges >= 0) {
+        PF_CHECK(a < nslab && nslab <= kSlabCache && (i_lo >= i_hi || (i_lo + c.ebase[a] >= 0 && i_hi + c.ebase[a] <= c.n_edges)));
         const CachedEdge* ed = c.edges + c.ebase[a];
         row_crossings_by([ed](int i, double y) { const CachedEdge& e = ed[i]; return x_at(e.x1, e.y1, e.x2, e.y2, y); },
                          py, x0, step, centre, n_pts, nw, words, i_lo, i_hi, c.e1[a]);
@@ -283,6 +284,7 @@ __device__ inline void fill_slab_cache(const PolyView& P, SlabCache& c, int ka, 
         if (j < nslab) c.ebase[j] = off - u0;
         if (j < nslab && off + cnt <= kEdgeCache)
             for (int t = 0; t < cnt; ++t) {
+                PF_CHECK(off + t < kEdgeCache);
                 const int e = __ldg(P.slab_edge + u0 + t);
                 c.edges[off + t] = CachedEdge{__ldg(P.edges + 4 * e), __ldg(P.edges + 4 * e + 1),
                                               __ldg(P.edges + 4 * e + 2), __ldg(P.edges + 4 * e + 3)};

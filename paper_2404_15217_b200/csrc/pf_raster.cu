@@ -54,6 +54,7 @@ __global__ void raster_mark_kernel(const void* blob, RasterHeader hdr, uint32_t*
             const int c0 = max(0, (int)ceil((xa - kEps - 1.0 - hdr.ox) * ic) - 1);
             const int c1 = min(hdr.nx - 1, (int)floor((xb + kEps + 1.0 - hdr.ox) * ic));
             uint32_t* row = words + (size_t)r * hdr.pitch;
+            PF_CHECK(r >= 0 && r < hdr.ny && (c1 < c0 || (c0 >= 0 && c1 < hdr.nx)));
             for (int c = c0; c <= c1; ++c) atomicOr(row + (c >> 4), 2u << (2 * (c & 15)));
         }
     }

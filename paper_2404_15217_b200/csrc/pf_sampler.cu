@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(kClassifyThreads) sample_classify_kernel(pf_sa
         if (lo >= k.need) atomicOr(ws.bitmaps + (size_t)s * (window / 32) + (a >> 5), 1u << (a & 31));
     } else {
         const uint32_t at = atomicAdd(reinterpret_cast<unsigned*>(ws.n_queue), 1u) - (uint32_t)kCountBase;
+        PF_CHECK(at < (uint32_t)cfg.n_slides * (uint32_t)window);
         ws.queue[at] = (int)q;
         ws.acc[at] = make_int2(0, 0);
     }
@@ -212,6 +213,7 @@ __device__ __forceinline__ void eval_part(const pf_sampler_config& cfg, const pf
     const uint32_t at = item / kEvalParts;
     const int part = (int)(item % kEvalParts);
     const uint32_t q = (uint32_t)__ldg(ws.queue + at);
+    PF_CHECK(q < (uint32_t)cfg.n_slides * (uint32_t)window);
     const int s = (int)(q / (uint32_t)window), a = (int)(q % (uint32_t)window);
     const pf_sampler_slide& sl = slides[s];
     const int4 cd = ws.cands[q];
@@ -311,6 +313,7 @@ __global__ void __launch_bounds__(kTableThreads) sample_table_kernel(pf_sampler_
         return;
     }
     const int sl = blockIdx.x;
+    PF_CHECK(words <= 2048);
     const uint32_t* bm = ws.bitmaps + (size_t)sl * words;
     for (int i = tid; i < words; i += kTableThreads) s_bm[i] = bm[i];
     __syncthreads();
@@ -509,6 +512,8 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
             // bitmaps, table and draws in three bulk copies (TMA) on one mbarrier, issued by one
             // thread: the per-thread copy loop of 98 KB was ~3 us of the walk
             n_fd = min(kFastDraws, 2 * (n - w.emitted) + 256);
+            PF_CHECK(((bm_bytes + 15) & ~15) + cfg.n_slides * window * 2 + kFastDraws * 4 + window * 4 <=
+                     (int)dynamic_smem_size());
             const uint32_t na_bytes = (uint32_t)cfg.n_slides * (uint32_t)window * 2u;
             const uint32_t fd_bytes = ((uint32_t)n_fd * 4u + 15u) & ~15u;
             const bool bm_bulk = (bm_bytes & 15) == 0;
