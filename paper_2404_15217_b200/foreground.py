@@ -123,11 +123,14 @@ class ForegroundPolygon:
         return blob
 
     def device_blob(self):
-        """Slab index resident in HBM (cached)."""
+        """Slab index resident in HBM (cached per device)."""
         torch = N.require_cuda()
+        dev = torch.cuda.current_device()
         if self._blob is None:
-            self._blob = torch.from_numpy(self.index_blob()).cuda()
-        return self._blob
+            self._blob = {}
+        if dev not in self._blob:
+            self._blob[dev] = torch.from_numpy(self.index_blob()).cuda()
+        return self._blob[dev]
 
     def device_raster(self, cell: float | None = None):
         """Classification raster of the polygon in HBM (pf_polygon_raster_build, cached): 2-bit
@@ -138,16 +141,16 @@ class ForegroundPolygon:
             cell = 32.0
             while ((bbox[2] - bbox[0]) / cell + 3) * ((bbox[3] - bbox[1]) / cell + 3) > (1 << 24):
                 cell *= 2.0
-        key = float(cell)
+        key = (torch.cuda.current_device(), float(cell))
         cache = getattr(self, "_rasters", None)
         if cache is None:
             cache = self._rasters = {}
         if key not in cache:
             nbytes = C.c_int64(0)
-            N.check(N.lib().pf_polygon_raster_bytes(bbox, key, C.byref(nbytes)), "pf_polygon_raster_bytes")
+            N.check(N.lib().pf_polygon_raster_bytes(bbox, key[1], C.byref(nbytes)), "pf_polygon_raster_bytes")
             out = torch.empty((nbytes.value,), dtype=torch.uint8, device="cuda")
             st = torch.cuda.current_stream()
-            N.check(N.lib().pf_polygon_raster_build(self.device_blob().data_ptr(), bbox, key, out.data_ptr(),
+            N.check(N.lib().pf_polygon_raster_build(self.device_blob().data_ptr(), bbox, key[1], out.data_ptr(),
                                                     nbytes.value, N.stream_ptr(st)), "pf_polygon_raster_build")
             cache[key] = out
         return cache[key]
