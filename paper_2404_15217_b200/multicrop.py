@@ -306,10 +306,6 @@ class MultiCropLoader:
         torch = N.require_cuda()
         torch.cuda.current_stream().wait_stream(self._side)
 
-    def kernels_per_batch(self) -> int:
-        """CUDA kernels one next_batch launches (sampler rounds + resample + params + 2 multi-crop groups)."""
-        smp = 1 + (4 * self.sampler.rounds if self.sampler.all_fit and self.sampler.rounds > 0 else 1)
-        return smp + (1 if self.needs_resample else 0) + 1 + (self.mc.n_global > 0) + (self.mc.n_local > 0)
 
 
 def _table(sampler):

@@ -299,11 +299,30 @@ class GpuSampler:
         w = int(n / p + 4.0 * math.sqrt(n * (1.0 - p)) / p) + 32
         return min(max(32, (w + 31) // 32 * 32), 1 << 16)
 
+    def _fits_table(self, window: int) -> bool:
+        """pf_sample's walk keeps a next-accept table in shared memory when it fits (pf_sampler.cu,
+        next_table): bitmaps + uint16 table + slide draws + emits <= 200 KB."""
+        words = window // 32
+        nt = (self.cfg.n_slides * words * 4 + 15) // 16 * 16 + self.cfg.n_slides * window * 2 + 8192 * 4 + window * 4
+        return window + self.cfg.max_attempts < 0x7FFF and nt <= 200 * 1024
+
     def next_batch(self, n: int, out=None, stream=None):
         """Next n specs of the stream as a device [n, 64] uint8 tensor; raises on stream failure lazily
-        (call ``check()`` or read ``specs_host``)."""
+        (call ``check()`` or read ``specs_host``).  A batch whose speculation window would not let
+        the walk keep its table in shared memory is sampled in consecutive sub-batches (the stream
+        is the same for any split)."""
         torch = N.require_cuda()
         st = stream if stream is not None else torch.cuda.current_stream()
+        if self.rounds > 0 and not self.window and n > 64 and not self._fits_table(self._window_for(n)):
+            with torch.cuda.stream(st):
+                if out is None:
+                    out = torch.empty((n, 64), dtype=torch.uint8, device="cuda")
+            k = n
+            while k > 64 and not self._fits_table(self._window_for(k)):
+                k = (k + 1) // 2
+            for i in range(0, n, k):
+                self.next_batch(min(k, n - i), out=out[i:i + k], stream=st)
+            return out
         window = self._window_for(n)
         nbytes = C.c_int64(0)
         N.check(N.lib().pf_sample_workspace_bytes(C.byref(self.cfg), window, C.byref(nbytes)), "pf_sample_workspace_bytes")
