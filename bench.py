@@ -558,6 +558,7 @@ def run_sweep(args, pf, plan, slides, rank, world, local, torch, dist, N):
                 for dtype in ("bf16", "f32"):
                     a = argparse.Namespace(**vars(args))
                     a.batch, a.dtype, a.steps, a.warmup = batch, dtype, max(3, min(args.steps, 5)), 3
+                    print(f"[sweep] patch {patch} batch {batch} L={n_local} {dtype}", file=sys.stderr, flush=True)
                     feed = make_feed(a, pf, plan, slides, rank, n_local=n_local, patch=patch)
                     elapsed_ms, stage_ms, launches, clocks = timed_run(feed, a, torch, dist, world, local, N)
                     st = feed.sampler.check()

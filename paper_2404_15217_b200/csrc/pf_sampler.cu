@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
     PF_WT(0);
     load_ws(state, w);
     if (w.status != PF_OK || w.emitted >= n) return;
+    const uint64_t m0_round = w.c_mpp;  // window offset 0 of this round's bitmaps
     const int tid = threadIdx.x, lane = tid & 31;
     const int max_att = cfg.max_attempts;
     const int64_t flimit = failure_limit(cfg);
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                     if (a >= wlim) {  // the window ends at this draw's first attempt
                         s = sj, used = 0, mid_draw = true;
                     } else {
-                        const int n_left = n - emitted;
+                        int n_left = n - emitted;  // specs still wanted when a fast segment starts
                         int32_t* el = semit + (emitted - s_first);
                         int k = 0;  // specs emitted by the fast loop
                         while (true) {
@@ -656,6 +657,7 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                                 break;
                             }
                             el = semit + (emitted - s_first);
+                            n_left = n - emitted;
                             sj = s_nxt;
                             row = na + (size_t)sj * window;
                             ++j;
@@ -682,8 +684,12 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
             }
             __syncthreads();
             if (tid < 32) load_ws(state, w);
-        } else if (tid < 32) {
-            const uint64_t m0 = w.c_mpp;
+        }
+        // general walk over the bitmaps: the whole round without a table, else whatever the fast
+        // walk's precomputed draws did not cover (its emits then continue in shared memory)
+        const bool fast_emits = next_table && s_fast;
+        if (tid < 32 && w.emitted < n && w.status == PF_OK) {
+            const uint64_t m0 = m0_round;
             const int wlim = min(window, *ws.reject_at);
             int draw_pos = kDrawCache, draw_cnt = kDrawCache;
             uint64_t draw_base = w.c_slide;  // counter of s_draw[0] is draw_base + 1
@@ -760,7 +766,11 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
                     w.c_mpp += consumed;
                     w.c_coords += 2ull * consumed;
                     w.attempts += consumed;
-                    if (lane == 0) emit_list[w.emitted - s_first] = make_int2(w.cur_slide, found);  // < window per round
+                    if (lane == 0) {  // < window per round
+                        PF_CHECK(w.emitted - s_first < window);
+                        if (fast_emits) semit[w.emitted - s_first] = (w.cur_slide << 16) | found;
+                        else emit_list[w.emitted - s_first] = make_int2(w.cur_slide, found);
+                    }
                     w.seq += 1;
                     w.emitted += 1;
                     w.failures = 0;
@@ -788,7 +798,6 @@ __global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(
         // materialise the emitted specs in parallel
         const int first = s_first, last = s_last;
         const int64_t seq0 = s_seq0;
-        const bool fast_emits = next_table && s_fast;
         for (int i = first + tid; i < last; i += kWalkThreads) {
             int2 e;
             if (fast_emits) {
@@ -915,7 +924,9 @@ extern "C" int pf_sample(const pf_sampler_config* cfg, const pf_sampler_slide* s
     // next-accepted-offset table beside the bitmaps (uint16 offsets: window < 0xffff)
     const size_t nt_bytes = (bm_bytes_all + 15) / 16 * 16 + (size_t)cfg->n_slides * window * 2 + (size_t)kFastDraws * 4 +
                             (size_t)window * 4;
-    const int next_table = bm_in_smem && window + cfg->max_attempts < 0x7fff && nt_bytes <= 200 * 1024;
+    // entries: f + 1 below the 0x4000 window-end mark (window <= 0x3fff), 0x8000 | a + M
+    const int next_table = bm_in_smem && window < 0x4000 && window + cfg->max_attempts < 0x7fff &&
+                           nt_bytes <= 200 * 1024;
     const size_t walk_smem = std::max((size_t)overlap_smem_bytes(cfg->grid),
                                       next_table ? nt_bytes : (bm_in_smem ? bm_bytes_all : (size_t)0));
     rc = check_cuda(cudaFuncSetAttribute(sample_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)walk_smem),

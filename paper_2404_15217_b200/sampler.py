@@ -304,7 +304,7 @@ class GpuSampler:
         next_table): bitmaps + uint16 table + slide draws + emits <= 200 KB."""
         words = window // 32
         nt = (self.cfg.n_slides * words * 4 + 15) // 16 * 16 + self.cfg.n_slides * window * 2 + 8192 * 4 + window * 4
-        return window + self.cfg.max_attempts < 0x7FFF and nt <= 200 * 1024
+        return window < 0x4000 and window + self.cfg.max_attempts < 0x7FFF and nt <= 200 * 1024
 
     def next_batch(self, n: int, out=None, stream=None):
         """Next n specs of the stream as a device [n, 64] uint8 tensor; raises on stream failure lazily

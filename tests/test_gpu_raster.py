@@ -172,3 +172,27 @@ def test_count_bounds_hold(polys):
         boundary = (count > 0) & (count < grid * grid)
         settled = boundary & ((b[:, 0] >= need) | (b[:, 1] < need))
         assert boundary.sum() > 50 and settled.sum() > 0.3 * boundary.sum()
+
+
+def test_large_batches_and_windows_keep_the_stream(polys):
+    """Batches of thousands of specs: split into sub-batches whose window keeps the walk's table
+    (entries below the 0x4000 mark), or walked over the bitmaps when a forced window is larger,
+    or sampled 1000 at a time -- the same stream."""
+    pf, ps = polys
+    import torch
+    from paper_2404_15217_b200.store import LevelInfo, SlideRecord
+
+    recs = [SlideRecord(f"c2_{g}", 0.25, 256, [LevelInfo(40000, 30000, 0.25, 1), LevelInfo(10000, 7500, 1.0, 4),
+                                               LevelInfo(2500, 1875, 4.0, 16)]) for g in range(2)]
+    cfg = pf.SamplerConfig(patch_size=224, seed=11, max_attempts_per_slide=8)
+    pairs = list(zip(recs, ps))
+    a = pf.GpuSampler(cfg, pairs, rounds=1)
+    b = pf.GpuSampler(cfg, pairs, rounds=1, window=20000)
+    c = pf.GpuSampler(cfg, pairs, rounds=2)
+    oa = a.next_batch(9000)
+    ob = b.next_batch(9000)
+    oc = torch.cat([c.next_batch(1000) for _ in range(9)])
+    torch.cuda.synchronize()
+    assert torch.equal(oa, ob) and torch.equal(oa, oc)
+    for s in (a, b, c):
+        s.check()

@@ -64,6 +64,21 @@ def test_long_stream_vs_oracle(pf, goldens):
         [(orc[si]["id"], x, y, fp, m, q) for si, x, y, fp, m, q in want]
 
 
+@pytest.mark.parametrize("batch", [64, 300])
+def test_stream_with_frequent_exhaustion_vs_oracle(pf, goldens, batch):
+    """max_attempts 3: draws exhaust in the middle of a batch, so the walk's table loop hands
+    over to its general step and back many times per call (a stale "specs still wanted" count
+    there once over-emitted); against the CPU oracle."""
+    slides = _slides(pf, goldens, [0, 1, 2])
+    cfg = pf.SamplerConfig(patch_size=32, epoch_size=300, seed=5, target_mpps=[(0.25, 1.0)], max_attempts_per_slide=3)
+    got = list(pf.epoch_stream(cfg, slides, batch=batch))
+    orc = [{"id": r.slide_id, "width": r.width, "height": r.height, "base_mpp": 0.25, "rings": p.rings} for r, p in slides]
+    want, _ = port.epoch_stream(orc, patch_size=32, min_fg=0.4, mpps=[(0.25, 1.0)], seed=5, epoch_size=300,
+                                max_attempts=3)
+    assert [(s.slide_id, s.x, s.y, s.width, s.target_mpp, s.seq) for s in got] == \
+        [(orc[si]["id"], x, y, fp, m, q) for si, x, y, fp, m, q in want]
+
+
 def test_specs_carry_read_plan(pf, goldens):
     c = goldens["epoch_streams"]["multi_mpp"]
     slides = _slides(pf, goldens, c["slides"])
