@@ -324,17 +324,38 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
     const int cpr = T * 3 / 16, c0 = a0 / 16;
     const int tx0 = c0 / cpr, e0 = c0 - tx0 * cpr;
     {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (int rr = warp; rr < nr; rr += kR2Threads / 32) {
+        // one TMA bulk copy per (staged row, tile the row crosses) on one mbarrier: per-16-byte
+        // cp.async with its tile address math was ~30 % of this kernel's instructions
+        __shared__ __align__(8) uint64_t s_bar;
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                         "r"((uint32_t)(nr * nch * 16))
+                         : "memory");
+        }
+        __syncthreads();  // armed before any copy completes on it
+        const int n_tiles = (e0 + nch + cpr - 1) / cpr;
+        for (int q = threadIdx.x; q < nr * n_tiles; q += kR2Threads) {
+            const int rr = q / n_tiles, t = q - rr * n_tiles;
             const int Y = sp.sy + R0 + rr;
             const int ty = Y / T, v = Y - ty * T;
-            for (int ch = lane; ch < nch; ch += 32) {
-                int e = e0 + ch, tx = tx0;
-                while (e >= cpr) e -= cpr, ++tx;  // a window row spans at most a few tiles
-                rr_cp_async16(stg + rr * pitch + ch * 16, tile_ptr(sd, L, tx, ty) + (size_t)v * T * 3 + e * 16);
-            }
+            const int ch0 = max(0, t * cpr - e0), ch1 = min(nch, (t + 1) * cpr - e0);
+            if (ch1 <= ch0) continue;
+            const uint8_t* src = tile_ptr(sd, L, tx0 + t, ty) + (size_t)v * T * 3 + (size_t)(e0 + ch0 - t * cpr) * 16;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    (uint32_t)__cvta_generic_to_shared(stg + rr * pitch + ch0 * 16)),
+                "l"(src), "r"((uint32_t)((ch1 - ch0) * 16)), "r"(bar)
+                : "memory");
         }
-        rr_cp_async_wait_all();
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}"
+                         : "=r"(done)
+                         : "r"(bar)
+                         : "memory");
     }
     __syncthreads();
     // horizontal pass: item = (staged row, 4 output columns): source pixels 2x0-1 .. 2x0+8 as
