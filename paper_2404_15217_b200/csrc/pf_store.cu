@@ -263,7 +263,10 @@ struct RROut<PF_BF16> {
 // taps, renormalised) take the table weights.  Bit-exact with the general path / Pillow.
 // Grid: (spec, band of kR2Rows output rows); specs it does not take exit at once.
 // ---------------------------------------------------------------------------
-constexpr int kR2Rows = 8;
+#ifndef PF_R2_ROWS
+#define PF_R2_ROWS 12  // measured: 4 rows 0.66 ms, 8 0.52, 12 0.49, 16 0.50, 24 0.53 per C3 read_regions call
+#endif
+constexpr int kR2Rows = PF_R2_ROWS;
 constexpr int kR2Threads = 256;
 
 __device__ __forceinline__ bool is_2x(const pf_patch_spec& sp, const pf_slide_desc& sd, int S) {
