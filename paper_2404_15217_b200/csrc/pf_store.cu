@@ -476,39 +476,22 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
     }
 }
 
+// One (spec, band) of the general read, block-uniform (every return leaves the item); `lut`
+// built by the caller.
 template <int kDtype>
-__global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide_desc* slides,
-                                                                  const pf_patch_spec* specs, int S, int layout,
-                                                                  int n_bands, NormParams np, void* out_v) {
+__device__ __forceinline__ void read_region_item(const pf_slide_desc* slides, const pf_patch_spec& sp, int spec_i,
+                                                 int band, int S, int layout,
+                                                 const typename RROut<kDtype>::T* lut, uint8_t* work, int work_bytes,
+                                                 void* out_v) {
     using OT = typename RROut<kDtype>::T;
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int spec_i = blockIdx.x / n_bands, band = blockIdx.x - spec_i * n_bands;
-    const pf_patch_spec sp = specs[spec_i];
-    const bool skip_pass = layout & PF_SKIP_PASSTHROUGH;
     const int lay = layout & 0xff;
     const pf_slide_desc& sd = slides[sp.slide];
     const int L = sp.level;
     const int LW = sd.width[L], LH = sd.height[L];
     const int side = sp.side;
     const bool pass = side == S;
-    if (pass && skip_pass) return;
     if (band * kRRBand >= S) return;
-    if (!pass && is_2x(sp, sd, S)) return;  // resample2x_kernel takes it
     OT* out = reinterpret_cast<OT*>(out_v);
-    // LUT for the epilogue
-    OT* lut = reinterpret_cast<OT*>(smem);
-    uint8_t* work = smem + ((3 * 256 * sizeof(OT) + 15) & ~size_t(15));
-    const int work_bytes = kRRSmem - (int)(work - smem);
-    for (int i = threadIdx.x; i < 3 * 256; i += kRRThreads) {
-        const int c = i >> 8;
-        const uint8_t v = (uint8_t)(i & 255);
-        if constexpr (kDtype == PF_U8) lut[i] = v;
-        else {
-            const float f = __fdiv_rn(__fdiv_rn((float)v, 255.0f) - np.mean[c], np.stdv[c]);
-            if constexpr (kDtype == PF_F32) lut[i] = f;
-            else lut[i] = __float2bfloat16_rn(f);
-        }
-    }
     const size_t plane = (size_t)S * S;
     OT* o = out + (size_t)spec_i * 3 * plane;
     const int T = sd.tile_size;
@@ -666,6 +649,42 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
             }
         }
         __syncthreads();
+    }
+}
+
+// Block = (spec, kRRBand-row band); with PF_SKIP_PASSTHROUGH (the multi-crop loaders: the
+// general path is then only for the rare resampled windows the exact 2:1 kernel cannot take)
+// a block takes a whole spec's bands, so the many specs other kernels take cost one block each
+// instead of n_bands.
+template <int kDtype>
+__global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide_desc* slides,
+                                                                  const pf_patch_spec* specs, int S, int layout,
+                                                                  int n_bands, NormParams np, void* out_v) {
+    using OT = typename RROut<kDtype>::T;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const bool per_spec = layout & PF_SKIP_PASSTHROUGH;
+    const int spec_i = per_spec ? (int)blockIdx.x : (int)blockIdx.x / n_bands;
+    const int band0 = per_spec ? 0 : (int)blockIdx.x - spec_i * n_bands;
+    const pf_patch_spec sp = specs[spec_i];
+    const bool pass = sp.side == S;
+    if (pass && per_spec) return;
+    if (!pass && is_2x(sp, slides[sp.slide], S)) return;  // resample2x_kernel takes it
+    OT* lut = reinterpret_cast<OT*>(smem);
+    uint8_t* work = smem + ((3 * 256 * sizeof(OT) + 15) & ~size_t(15));
+    const int work_bytes = kRRSmem - (int)(work - smem);
+    for (int i = threadIdx.x; i < 3 * 256; i += kRRThreads) {
+        const int c = i >> 8;
+        const uint8_t v = (uint8_t)(i & 255);
+        if constexpr (kDtype == PF_U8) lut[i] = v;
+        else {
+            const float f = __fdiv_rn(__fdiv_rn((float)v, 255.0f) - np.mean[c], np.stdv[c]);
+            if constexpr (kDtype == PF_F32) lut[i] = f;
+            else lut[i] = __float2bfloat16_rn(f);
+        }
+    }
+    for (int band = band0; band < (per_spec ? n_bands : band0 + 1); ++band) {
+        read_region_item<kDtype>(slides, sp, spec_i, band, S, layout, lut, work, work_bytes, out_v);
+        __syncthreads();  // the band's staging / planes are reused by the next
     }
 }
 
@@ -853,7 +872,7 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
     // every spec is split into kRRBand-row output bands across CTAs (passthrough and PIL resample
     // alike); with PF_SKIP_PASSTHROUGH the passthrough specs' CTAs exit at once
     const int n_bands = (out_size + kRRBand - 1) / kRRBand;
-    const long long grid = (long long)n * n_bands;
+    const long long grid = (layout & PF_SKIP_PASSTHROUGH) ? (long long)n : (long long)n * n_bands;
     cudaStream_t st = as_stream(stream);
     int rc;
     // the exact 2:1 kernel's shared memory: LUT + (2 * kR2Rows + 2) staged rows + planar H output
