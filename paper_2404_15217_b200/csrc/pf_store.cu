@@ -267,6 +267,10 @@ struct RROut<PF_BF16> {
 #define PF_R2_ROWS 12  // measured: 4 rows 0.66 ms, 8 0.52, 12 0.49, 16 0.50, 24 0.53 per C3 read_regions call
 #endif
 constexpr int kR2Rows = PF_R2_ROWS;
+#ifndef PF_R2_BANDS
+#define PF_R2_BANDS 1
+#endif
+constexpr int kR2Bands = PF_R2_BANDS;  // bands per block
 constexpr int kR2Threads = 256;
 
 __device__ __forceinline__ bool is_2x(const pf_patch_spec& sp, const pf_slide_desc& sd, int S) {
@@ -288,12 +292,12 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
     using OT = typename RROut<kDtype>::T;
     const int S = kS ? kS : S_rt;  // compile-time for the BASELINE size: index math without divisions
     extern __shared__ __align__(16) uint8_t smem[];
-    const int spec_i = blockIdx.x / n_bands, band = blockIdx.x - spec_i * n_bands;
+    // block = (spec, group of kR2Bands bands, taken one after the other)
+    const int n_groups = (n_bands + kR2Bands - 1) / kR2Bands;
+    const int spec_i = blockIdx.x / n_groups, group = blockIdx.x - spec_i * n_groups;
     const pf_patch_spec sp = specs[spec_i];
     const pf_slide_desc& sd = slides[sp.slide];
     if (!is_2x(sp, sd, S)) return;
-    const int Y0 = band * kR2Rows, Y1 = min(S, Y0 + kR2Rows);
-    if (Y0 >= S) return;
     const int lay = layout & 0xff;
     const int L = sp.level, T = sd.tile_size;
     const int side = 2 * S;
@@ -315,6 +319,19 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
             if constexpr (kDtype == PF_F32) lut[i] = f;
             else lut[i] = __float2bfloat16_rn(f);
         }
+    // one TMA bulk copy per (staged row, tile the row crosses) on one mbarrier (phase per band):
+    // per-16-byte cp.async with its tile address math was ~30 % of this kernel's instructions
+    __shared__ __align__(8) uint64_t s_bar;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();  // initialised before any copy completes on it
+    for (int it = 0; it < kR2Bands; ++it) {
+    const int band = group * kR2Bands + it;
+    const int Y0 = band * kR2Rows, Y1 = min(S, Y0 + kR2Rows);
+    if (Y0 >= S) break;
     // source rows of the band: output y uses rows 2y - 1 .. 2y + 2 (y = 0: 0..2; y = S-1: 2S-3..2S-1)
     const int R0 = max(0, 2 * Y0 - 1), R1 = min(side, 2 * (Y1 - 1) + 3);
     const int nr = R1 - R0;
@@ -327,18 +344,12 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
     const int cpr = T * 3 / 16, c0 = a0 / 16;
     const int tx0 = c0 / cpr, e0 = c0 - tx0 * cpr;
     {
-        // one TMA bulk copy per (staged row, tile the row crosses) on one mbarrier: per-16-byte
-        // cp.async with its tile address math was ~30 % of this kernel's instructions
-        __shared__ __align__(8) uint64_t s_bar;
-        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
-        if (threadIdx.x == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // the arrive (thread 0) keeps the phase open until it has happened, so copies that
+        // complete before it only take the transaction count negative
+        if (threadIdx.x == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                          "r"((uint32_t)(nr * nch * 16))
                          : "memory");
-        }
-        __syncthreads();  // armed before any copy completes on it
         const int n_tiles = (e0 + nch + cpr - 1) / cpr;
         for (int q = threadIdx.x; q < nr * n_tiles; q += kR2Threads) {
             const int rr = q / n_tiles, t = q - rr * n_tiles;
@@ -355,9 +366,9 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
         }
         uint32_t done = 0;
         while (!done)
-            asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}"
+            asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
                          : "=r"(done)
-                         : "r"(bar)
+                         : "r"(bar), "r"((uint32_t)(it & 1))
                          : "memory");
     }
     __syncthreads();
@@ -473,6 +484,8 @@ __global__ void __launch_bounds__(kR2Threads) resample2x_kernel(const pf_slide_d
                     else o[idx] = lut[c * 256 + v];
                 }
         }
+    }
+    __syncthreads();  // the next band restages the buffers
     }
 }
 
@@ -879,6 +892,7 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
     const int r2_rows = 2 * kR2Rows + 2;
     const int r2_smem = 3 * 256 * 4 + r2_rows * ((15 + 6 * out_size + 15) / 16 * 16 + 16) + 3 * r2_rows * out_size + 64;
     const int r2_bands = (out_size + kR2Rows - 1) / kR2Rows;
+    const int r2_groups = (r2_bands + kR2Bands - 1) / kR2Bands;
     const bool r2 = r2_smem <= 160 * 1024;
 #define PF_RR_LAUNCH(DT)                                                                                          \
     rc = check_cuda(cudaFuncSetAttribute(read_regions_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
@@ -894,14 +908,14 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, r2_smem),           \
                             "cudaFuncSetAttribute");                                                              \
             if (rc) return rc;                                                                                    \
-            resample2x_kernel<DT, 224><<<(unsigned)((long long)n * r2_bands), kR2Threads, r2_smem, st>>>(         \
+            resample2x_kernel<DT, 224><<<(unsigned)((long long)n * r2_groups), kR2Threads, r2_smem, st>>>(        \
                 slides_dev, specs_dev, out_size, layout, r2_bands, np, out);                                      \
         } else {                                                                                                  \
             rc = check_cuda(cudaFuncSetAttribute(resample2x_kernel<DT, 0>,                                        \
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, r2_smem),           \
                             "cudaFuncSetAttribute");                                                              \
             if (rc) return rc;                                                                                    \
-            resample2x_kernel<DT, 0><<<(unsigned)((long long)n * r2_bands), kR2Threads, r2_smem, st>>>(           \
+            resample2x_kernel<DT, 0><<<(unsigned)((long long)n * r2_groups), kR2Threads, r2_smem, st>>>(          \
                 slides_dev, specs_dev, out_size, layout, r2_bands, np, out);                                      \
         }                                                                                                         \
     }
