@@ -194,3 +194,25 @@ def test_f32_and_bf16_outputs_agree_with_u8(pf, scene):
     for u8, f32 in ((g8, gf), (l8, lf)):
         want = (u8.cpu().numpy().astype(np.float32) / np.float32(255.0) - mean) / std
         assert np.array_equal(f32.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_random_configs_vs_torchvision(pf, scene, case):
+    """Random multi-crop configurations (crop counts and sizes across the compile-time and
+    generic kernel paths -- sizes down to src/3.5, the resample's tap limit -- scale/ratio ranges, jitter strengths, op probabilities, solarize
+    threshold) against torchvision on the same parameters: <= 1 LSB, < 0.1 % of values."""
+    rs = np.random.default_rng(500 + case)
+    n_global = int(rs.integers(1, 3))
+    n_local = int(rs.choice([0, 2, 4, 8]))
+    n = n_global + n_local
+    lo = float(rs.uniform(0.08, 0.5))
+    cfg = pf.mc.MultiCropConfig(
+        n_global=n_global, n_local=n_local,
+        global_size=int(rs.choice([224, 192, 160])), local_size=int(rs.choice([96, 112, 128])),
+        global_scale=(lo, 1.0), local_scale=(0.05, lo), ratio=(float(rs.uniform(0.5, 0.9)), float(rs.uniform(1.1, 2.0))),
+        p_flip=float(rs.uniform()), p_jitter=float(rs.uniform(0.5, 1.0)), p_gray=float(rs.uniform(0, 0.5)),
+        brightness=float(rs.uniform(0, 0.6)), contrast=float(rs.uniform(0, 0.6)), saturation=float(rs.uniform(0, 0.6)),
+        hue=float(rs.uniform(0, 0.5)), p_blur=[float(v) for v in rs.uniform(0, 1, n)],
+        p_solarize=[float(v) for v in rs.uniform(0, 0.5, n)], solarize_threshold=float(rs.choice([64.0, 128.0, 200.5])))
+    worst, frac = _check_against_torchvision(pf, scene, cfg)
+    assert frac < 1e-3, (frac, cfg)
