@@ -116,7 +116,12 @@ def read_region(levels, mpps, downsamples, rect, target_mpp: float, out_size: in
     """Slide.read_region (store.py:651-688) over in-memory levels (PIL resize as the reference)."""
     from PIL import Image
 
-    x, y, _w, _h = rect
+    x, y, w, h = rect
+    if out_size < 1:
+        raise ValueError("out_size must be >= 1")
+    lw, lh = levels[0].shape[1], levels[0].shape[0]
+    if w < 1 or h < 1 or x < 0 or y < 0 or x + w > lw or y + h > lh:  # store.py:668-675
+        raise IndexError(f"rect {tuple(rect)} outside level-0 bounds {lw}x{lh}")
     li = select_level(mpps, target_mpp)
     side = max(1, round_half_away(out_size * target_mpp / mpps[li]))
     sx, sy = round_half_away(x / downsamples[li]), round_half_away(y / downsamples[li])

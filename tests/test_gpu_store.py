@@ -179,3 +179,43 @@ def test_resample_2x_fast_path_exact(pf, cuda):
         assert np.array_equal(ss.read_regions(specs, out).cpu().numpy(), want), out
         f32 = ss.read_regions(specs, out, dtype="f32", layout="nchw").cpu().numpy()
         assert np.array_equal(f32, port.normalize_patch(want).transpose(0, 3, 1, 2)), out
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_random_reads_vs_oracle(pf, case):
+    """Random windows (edges and overruns included), target mpps, output sizes, dtypes and
+    layouts through the batched device read and the drop-in read_region, against the oracle's
+    read_region (PIL) + normalize_patch: bit-exact, OutOfBoundsError where the reference raises."""
+    rs = np.random.default_rng(700 + case)
+    H, W = int(rs.integers(300, 900)), int(rs.integers(300, 900))
+    img = rs.integers(0, 256, size=(H, W, 3), dtype=np.uint8)
+    T = int(rs.choice([64, 128, 256]))
+    f = int(rs.choice([2, 4]))
+    s = pf.GpuSlide.from_array(img, f"r{case}", 0.25, tile_size=T, downsample_factor=f)
+    ss = pf.SlideSet([s])
+    lv = port.pyramid(img, T, f)
+    mpps = [x.mpp for x in s.record.levels]
+    ds = [x.downsample for x in s.record.levels]
+    reqs, wants = [], []
+    for _ in range(40):
+        mpp = float(rs.choice([0.25, 0.3, 0.5, 0.7, 1.0, 2.0]))
+        out = int(rs.choice([8, 32, 96, 224, 300]))
+        side = int(rs.integers(4, min(H, W)))
+        x, y = int(rs.integers(-2, W - side + 3)), int(rs.integers(-2, H - side + 3))
+        try:
+            want = port.read_region(lv, mpps, ds, (x, y, side, side), mpp, out)
+        except IndexError:
+            with pytest.raises(pf.OutOfBoundsError):
+                s.read_region((x, y, side, side), mpp, out)
+            continue
+        got = s.read_region((x, y, side, side), mpp, out)
+        assert np.array_equal(got, want), (x, y, side, mpp, out)
+        if out == 96:
+            reqs.append((0, (x, y, side, side), mpp, 96))
+            wants.append(want)
+    if reqs:  # the same windows batched, every dtype and layout
+        specs = pf.store.plan_specs(reqs, ss.records)
+        want = np.stack(wants)
+        assert np.array_equal(ss.read_regions(specs, 96).cpu().numpy(), want)
+        f32 = ss.read_regions(specs, 96, dtype="f32", layout="nchw").cpu().numpy()
+        assert np.array_equal(f32, port.normalize_patch(want).transpose(0, 3, 1, 2))
