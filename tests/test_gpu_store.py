@@ -1,6 +1,8 @@
 """GPU parity: pyramid build, thumbnails, read_region (gather + PIL resample) and normalisation
 against the oracle and the reference goldens.  Bit-exact (integer / byte work)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -181,7 +183,7 @@ def test_resample_2x_fast_path_exact(pf, cuda):
         assert np.array_equal(f32, port.normalize_patch(want).transpose(0, 3, 1, 2)), out
 
 
-@pytest.mark.parametrize("case", range(4))
+@pytest.mark.parametrize("case", range(int(os.environ.get("PF_FUZZ_CASES_RR", "4"))))
 def test_random_reads_vs_oracle(pf, case):
     """Random windows (edges and overruns included), target mpps, output sizes, dtypes and
     layouts through the batched device read and the drop-in read_region, against the oracle's
