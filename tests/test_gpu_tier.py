@@ -94,3 +94,24 @@ def test_resize_pool_under_a_live_loader(pf, cuda):
         torch.cuda.synchronize()
         b.check()
         assert torch.equal(oa["global_crops"], ob["global_crops"]) and torch.equal(oa["local_crops"], ob["local_crops"])
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_random_pools_and_batches_match_dense(pf, cuda, case):
+    """Random pool fractions, batch sizes and sampler seeds over many batches (evictions every
+    step): crops byte-identical to the dense slides and no fault."""
+    torch = cuda
+    rs = np.random.default_rng(40 + case)
+    seed = int(rs.integers(20, 1000))
+    d, _, poly = _slide_and_poly(pf, seed, sid=f"d{seed}")
+    t, poly_t, st, n0 = _tiered(pf, seed, float(rs.uniform(0.3, 0.6)))
+    batch = int(rs.choice([16, 32, 48]))
+    cfg = pf.SamplerConfig(patch_size=224, seed=int(rs.integers(0, 1 << 20)), target_mpps=[(0.25, 1.0), (0.5, 1.0)])
+    a = pf.mc.MultiCropLoader([(d, poly)], cfg, batch_size=batch, dtype="u8")
+    b = pf.mc.MultiCropLoader([(t, poly_t)], cfg, batch_size=batch, dtype="u8")
+    for _ in range(10):
+        oa, ob = a.next_batch(), b.next_batch()
+        torch.cuda.synchronize()
+        assert torch.equal(oa["global_crops"], ob["global_crops"]) and torch.equal(oa["local_crops"], ob["local_crops"])
+    b.check()
+    assert st.tiles_filled() > 0
