@@ -179,3 +179,29 @@ def test_torch_aa_taps_never_need_the_uint8_clamp(out_size):
         for taps in q:
             assert min(taps, default=0) >= 0
             assert 255 * sum(taps) + (1 << (p - 1)) < (1 << (p + 8)), (in_size, out_size)
+
+
+@pytest.mark.parametrize("out_size", [16, 96, 112, 224])
+def test_taps_rescaled_to_precision_16_give_the_same_bytes(out_size):
+    """pf_multicrop.cu kAlignNote: for precision p <= 16 the tables hold the taps shifted to
+    precision 16 (u16, a lone 1.0 tap at p = 14 stored as 65535), and the resample's result byte
+    (sum w v + 2^(p-1)) >> p is unchanged for every crop extent and every uint8 input; an
+    output whose 1.0 tap shares the row with another non-zero tap (which keeps its precision)
+    never occurs."""
+    rs = np.random.default_rng(out_size)
+    for in_size in range(1, min(224, int(3.5 * out_size)) + 1):
+        _, q, p = port.aa_axis_table(in_size, out_size, "torch")
+        if p > 16:
+            continue
+        for taps in q:
+            taps = [int(t) for t in taps]
+            nz = sum(t != 0 for t in taps)
+            assert not (p == 14 and (1 << 14) in taps and nz > 1), (in_size, out_size)
+            w16 = [min(t << (16 - p), 65535) for t in taps]
+            assert max(w16, default=0) <= 65535
+            vals = rs.integers(0, 256, size=(64, len(taps)))
+            vals[0] = 255
+            vals[1] = 0
+            want = ((vals * np.array(taps)).sum(1) + (1 << (p - 1))) >> p
+            got = ((vals * np.array(w16)).sum(1) + (1 << 15)) >> 16
+            assert np.array_equal(want, got), (in_size, out_size, taps)
