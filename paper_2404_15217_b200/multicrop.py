@@ -196,7 +196,11 @@ class MultiCropLoader:
         self._ready = [None, None]
         self._free = [torch.cuda.Event(), torch.cuda.Event()]
         self._next_slot = 0
-        self.params = torch.empty((batch_size, self.mc.n_crops, 64), dtype=torch.uint8, device="cuda")
+        # crop parameters depend on (seed, rank, step) only, so each slot's are computed with its
+        # specs (on the side stream under prefetch) instead of between two steps on the main stream
+        self.params_slots = [torch.empty((batch_size, self.mc.n_crops, 64), dtype=torch.uint8, device="cuda")
+                             for _ in range(2)]
+        self.params = self.params_slots[0]
         # resampled sources, one per slot: the next step's PIL resample runs on the side stream
         # right after its sampler, under this step's multi-crop (memory-bound beside issue-bound)
         self.src_slots = ([torch.empty((batch_size, S, S, 3), dtype=torch.uint8, device="cuda") for _ in range(2)]
@@ -215,11 +219,12 @@ class MultiCropLoader:
         ts = TierSet(self.slide_set)
         self.tiers = ts if ts.active else None
 
-    def _sample(self, slot: int, st) -> None:
-        """Specs of a slot, their tiles made resident (tiered slides) and, when some mpp needs it,
-        their resampled S x S sources -- all on stream ``st``."""
+    def _sample(self, slot: int, st, step: int) -> None:
+        """Specs of a slot, their tiles made resident (tiered slides), when some mpp needs it
+        their resampled S x S sources, and the crop parameters of ``step`` -- all on stream ``st``."""
         torch = N.require_cuda()
         self.specs_from.next_batch(self.batch_size, out=self.specs_slots[slot], stream=st)
+        crop_params(self.mc, self.batch_size, self.seed, self.rank, step, out=self.params_slots[slot], stream=st)
         if self.tiers is not None:
             self.tiers.prefetch(self.specs_slots[slot], self.batch_size, stream=st)
         if self.needs_resample:
@@ -253,14 +258,14 @@ class MultiCropLoader:
         n = self.batch_size
         mark("begin")
         if not self.prefetch:
-            self._sample(0, st)
+            self._sample(0, st, self.step)
             cur = 0
             mark("sample")
         else:
             cur = self._next_slot
             if self._ready[cur] is None:  # first step: nothing prefetched yet
                 self._side.wait_stream(st)
-                self._sample(cur, self._side)
+                self._sample(cur, self._side, self.step)
                 self._ready[cur] = torch.cuda.Event()
                 self._ready[cur].record(self._side)
             st.wait_event(self._ready[cur])
@@ -272,14 +277,12 @@ class MultiCropLoader:
         specs = self.specs_slots[cur]
         src = self.src_slots[cur]
         res_ev = self._res_ev[cur]
-        # the crop parameters are launched before the next step's sampler so that the sampler's
-        # speculative-evaluation blocks do not take the SMs first
-        crop_params(self.mc, n, self.seed, self.rank, self.step, out=self.params, stream=st)
+        self.params = self.params_slots[cur]  # computed with this slot's specs
         mark("params")
         if self.prefetch:
             nxt = 1 - cur
             self._side.wait_event(self._free[nxt])  # step k-1 finished reading that slot
-            self._sample(nxt, self._side)
+            self._sample(nxt, self._side, self.step + 1)
             self._ready[nxt] = torch.cuda.Event()
             self._ready[nxt].record(self._side)
             self._next_slot = nxt
