@@ -248,7 +248,7 @@ def make_feed(args, pf, plan, slides, rank, src_size=224, n_local=8, patch=224):
         bpp = 224 * 224 * 3 + 224 * 224 * 3 * el
         wl = (f"C1: {args.slides} slide {args.width}x{args.height} in HBM, sat>0.07+morph mask on 1/32 thumbnail, "
               f"epoch_stream sampler 224px min_fg 0.40, read_region + ImageNet normalise to {args.dtype} NCHW")
-        return Feed(loader, "read", bpp, "read_regions_kernel", wl, run_e2e_regions)
+        return Feed(loader, "read", bpp, "passthrough_kernel (pf_read_regions with PF_SKIP_RESAMPLED)", wl, run_e2e_regions)
     mpps = [(0.25, 1.0), (0.5, 1.0), (1.0, 1.0), (2.0, 1.0)] if args.config == "3" else [(0.25, 1.0)]
     if args.config == "5":
         mpps = [(0.25 * patch / 224.0, 1.0)]

@@ -51,6 +51,10 @@ enum pf_dtype { PF_U8 = 0, PF_F32 = 1, PF_BF16 = 2 };
  * reads those straight from the pyramid). */
 enum pf_layout { PF_HWC = 0, PF_NCHW = 1 };
 #define PF_SKIP_PASSTHROUGH 256
+/* OR with PF_SKIP_RESAMPLED to leave the output of specs with side != out_size
+ * untouched: when every spec is a passthrough (the caller's target mpps all map
+ * to side == out_size) a lean passthrough kernel serves the call. */
+#define PF_SKIP_RESAMPLED 512
 
 /* Tissue-mask rules for pf_mask. */
 enum pf_mask_mode {

@@ -36,6 +36,7 @@ PF_ERR_DECODE = 10
 PF_U8, PF_F32, PF_BF16 = 0, 1, 2
 PF_HWC, PF_NCHW = 0, 1
 PF_SKIP_PASSTHROUGH = 256
+PF_SKIP_RESAMPLED = 512
 PF_MASK_LUMINANCE, PF_MASK_SATURATION = 0, 1
 
 PF_AUG_FLIP, PF_AUG_JITTER, PF_AUG_GRAY, PF_AUG_BLUR, PF_AUG_SOLARIZE = 1, 2, 4, 8, 16

@@ -237,6 +237,11 @@ class RegionLoader:
         tdt = {"u8": torch.uint8, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
         shape = (batch_size, 3, S, S) if layout == "nchw" else (batch_size, S, S, 3)
         self.out = torch.empty(shape, dtype=tdt, device="cuda")
+        # every (slide, target mpp) reads its window unresampled: the lean passthrough kernel
+        raw = self.sampler.slides_dev.cpu().numpy().tobytes()
+        size = N.C.sizeof(N.SamplerSlide)
+        table = [N.SamplerSlide.from_buffer_copy(raw[i * size:(i + 1) * size]) for i in range(len(raw) // size)]
+        self.passthrough_only = all(int(t.side[k]) == S for t in table for k in range(len(sampler_config.target_mpps)))
 
     def next_batch(self, stream=None, marks: list | None = None):
         torch = N.require_cuda()
@@ -272,7 +277,8 @@ class RegionLoader:
                 self._ready[nxt].record(self._side)
         specs = self.specs_slots[cur][pos * n:(pos + 1) * n]
         self.slide_set.read_regions(specs, self.out_size, dtype=self.dtype, layout=self.layout,
-                                    mean=self.mean, std=self.std, out=self.out, stream=st, planned=True)
+                                    mean=self.mean, std=self.std, out=self.out, stream=st, planned=True,
+                                    passthrough_only=self.passthrough_only)
         mark("read")
         if self.prefetch:
             self._pos = pos + 1

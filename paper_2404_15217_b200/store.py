@@ -777,11 +777,15 @@ class SlideSet:
         return torch.from_numpy(arr.view(np.uint8).reshape(len(arr), 64)).cuda(non_blocking=False)
 
     def read_regions(self, specs, out_size: int, *, dtype: str = "u8", layout: str = "hwc", mean=(0.5, 0.5, 0.5),
-                     std=(0.5, 0.5, 0.5), out=None, stream=None, planned: bool = False):
+                     std=(0.5, 0.5, 0.5), out=None, stream=None, planned: bool = False,
+                     passthrough_only: bool = False):
         """Batched read_region on device -> tensor [n, S, S, 3] (hwc) or [n, 3, S, S] (nchw).
 
         dtype "u8" returns raw pixels; "f32"/"bf16" apply (v/255 - mean)/std
         (normalize_patch, pkg/pipeline.py:152-155, for mean = std = 0.5).
+        ``passthrough_only``: the caller knows every spec reads its window unresampled
+        (side == out_size); the lean passthrough kernel serves the call (PF_SKIP_RESAMPLED:
+        a resampled spec's output would be left untouched).
         """
         torch = N.require_cuda()
         dspecs = self.specs_to_device(specs)
@@ -790,6 +794,7 @@ class SlideSet:
         code, tdt = dt[dtype]
         lay = {"hwc": N.PF_HWC, "nchw": N.PF_NCHW}[layout]
         shape = (n, out_size, out_size, 3) if lay == N.PF_HWC else (n, 3, out_size, out_size)
+        flags = N.PF_SKIP_RESAMPLED if passthrough_only else 0
         if out is None:
             out = torch.empty(shape, dtype=tdt, device="cuda")
         sp = N.stream_ptr(stream)
@@ -811,7 +816,7 @@ class SlideSet:
         if not planned:
             N.check(N.lib().pf_plan_regions(self.descs.data_ptr(), dspecs.data_ptr(), n, sp), "pf_plan_regions")
         N.check(
-            N.lib().pf_read_regions(self.descs.data_ptr(), dspecs.data_ptr(), n, out_size, code, lay,
+            N.lib().pf_read_regions(self.descs.data_ptr(), dspecs.data_ptr(), n, out_size, code, lay | flags,
                                     N.C.cast(m, N.C.c_void_p), N.C.cast(s, N.C.c_void_p), out.data_ptr(), sp),
             "pf_read_regions",
         )

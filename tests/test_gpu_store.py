@@ -221,3 +221,33 @@ def test_random_reads_vs_oracle(pf, case):
         assert np.array_equal(ss.read_regions(specs, 96).cpu().numpy(), want)
         f32 = ss.read_regions(specs, 96, dtype="f32", layout="nchw").cpu().numpy()
         assert np.array_equal(f32, port.normalize_patch(want).transpose(0, 3, 1, 2))
+
+
+def test_passthrough_only_reads_match_the_general_kernel(pf):
+    """PF_SKIP_RESAMPLED (RegionLoader when every target mpp reads its window unresampled): the
+    lean passthrough kernel's output equals read_regions_kernel's for every dtype and layout,
+    windows at the level edges (edge replication) included, and a resampled spec in the batch
+    is left untouched."""
+    import torch
+
+    rs = np.random.default_rng(41)
+    H, W = 700, 900
+    img = rs.integers(0, 256, size=(H, W, 3), dtype=np.uint8)
+    # tile 120: rows of 360 B are not 16-byte multiples, so slide 1 takes the per-pixel staging path
+    ss = pf.SlideSet([pf.GpuSlide.from_array(img, "pt", 0.25, tile_size=128, downsample_factor=4),
+                      pf.GpuSlide.from_array(img, "pt120", 0.25, tile_size=120, downsample_factor=4)])
+    for S in (224, 96, 300):
+        reqs = [(int(rs.integers(0, 2)), (int(rs.integers(0, W - S)), int(rs.integers(0, H - S)), S, S), 0.25, S)
+                for _ in range(21)]
+        reqs += [(0, (0, 0, S, S), 0.25, S), (0, (W - S, H - S, S, S), 0.25, S)]  # windows at the edges
+        specs = pf.store.plan_specs(reqs, ss.records)
+        for dtype, layout in (("f32", "nchw"), ("bf16", "nchw"), ("u8", "nchw"), ("u8", "hwc"), ("f32", "hwc")):
+            want = ss.read_regions(specs, S, dtype=dtype, layout=layout).cpu()
+            got = ss.read_regions(specs, S, dtype=dtype, layout=layout, passthrough_only=True).cpu()
+            assert torch.equal(got, want), (S, dtype, layout)
+        # a resampled spec (side != S) is left as it was
+        mixed = pf.store.plan_specs(reqs[:3] + [(0, (10, 10, 2 * S, 2 * S), 0.5, S)], ss.records)
+        sentinel = torch.full((4, 3, S, S), -7.0, device="cuda")
+        ss.read_regions(mixed, S, dtype="f32", layout="nchw", out=sentinel, passthrough_only=True)
+        ref = ss.read_regions(mixed, S, dtype="f32", layout="nchw").cpu()
+        assert torch.equal(sentinel[:3].cpu(), ref[:3]) and bool((sentinel[3] == -7.0).all())
