@@ -723,12 +723,17 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
 }
 
 // PF_SKIP_RESAMPLED launches (every spec a passthrough, e.g. BASELINE config 1): a lean
-// kernel of kPTBand-row bands with only the band's staged rows in shared memory (~11 KB: 8
+// kernel of kPTBand-row bands with only the band's staged rows in shared memory (~19 KB at 224 px: 8
 // CTAs per SM instead of read_regions_kernel's 2) and the normalising LUT read from a global
-// table through L1 instead of 768 divided entries built per CTA.  (Measured: 8-row bands 7 %
-// slower, 32-row bands equal; a persistent grid double-buffering the next band's rows no
-// faster.)
-constexpr int kPTBand = 16;
+// table through L1 instead of 768 divided entries built per CTA.  28-row bands (8 per 224 px
+// patch: 2048 CTAs for C1's 256 patches, ~19 KB so still 8 CTAs per SM) measured 4 % faster than
+// 16 (C1 4.04 -> 4.21 M patches/s); 12, 20, 24 and 32 rows no better than 16, and 32 rows exceed
+// the 48 KB default dynamic shared memory at out_size 512.  Streaming (.cs) stores: neutral.  A
+// persistent grid double-buffering the next band's rows was no faster.
+#ifndef PF_PT_BAND
+#define PF_PT_BAND 28
+#endif
+constexpr int kPTBand = PF_PT_BAND;
 template <int kDtype>
 __global__ void __launch_bounds__(256) passthrough_kernel(const pf_slide_desc* slides, const pf_patch_spec* specs,
                                                           int S, int layout, int n_bands,
@@ -978,7 +983,7 @@ extern "C" int pf_read_regions(const pf_slide_desc* slides_dev, const pf_patch_s
             lut = it->second;
         }
         const int nbp = (out_size + kPTBand - 1) / kPTBand;
-        const int smem = kPTBand * (((15 + out_size * 3 + 15) & ~15) + 16);  // <= 25 KB (out_size <= 512)
+        const int smem = kPTBand * (((15 + out_size * 3 + 15) & ~15) + 16);  // <= 44 KB (out_size <= 512)
         const unsigned grid = (unsigned)((long long)n * nbp);
         switch (dtype) {
             case PF_U8:

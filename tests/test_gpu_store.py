@@ -236,7 +236,7 @@ def test_passthrough_only_reads_match_the_general_kernel(pf):
     # tile 120: rows of 360 B are not 16-byte multiples, so slide 1 takes the per-pixel staging path
     ss = pf.SlideSet([pf.GpuSlide.from_array(img, "pt", 0.25, tile_size=128, downsample_factor=4),
                       pf.GpuSlide.from_array(img, "pt120", 0.25, tile_size=120, downsample_factor=4)])
-    for S in (224, 96, 300):
+    for S in (224, 96, 300, 512):  # 512: the largest out_size, the most shared memory per band
         reqs = [(int(rs.integers(0, 2)), (int(rs.integers(0, W - S)), int(rs.integers(0, H - S)), S, S), 0.25, S)
                 for _ in range(21)]
         reqs += [(0, (0, 0, S, S), 0.25, S), (0, (W - S, H - S, S, S), 0.25, S)]  # windows at the edges
@@ -246,7 +246,8 @@ def test_passthrough_only_reads_match_the_general_kernel(pf):
             got = ss.read_regions(specs, S, dtype=dtype, layout=layout, passthrough_only=True).cpu()
             assert torch.equal(got, want), (S, dtype, layout)
         # a resampled spec (side != S) is left as it was
-        mixed = pf.store.plan_specs(reqs[:3] + [(0, (10, 10, 2 * S, 2 * S), 0.5, S)], ss.records)
+        r, mpp = (2 * S, 0.5) if S < 512 else (600, 0.3)  # a window that fits the 900 x 700 slide
+        mixed = pf.store.plan_specs(reqs[:3] + [(0, (10, 10, r, r), mpp, S)], ss.records)
         sentinel = torch.full((4, 3, S, S), -7.0, device="cuda")
         ss.read_regions(mixed, S, dtype="f32", layout="nchw", out=sentinel, passthrough_only=True)
         ref = ss.read_regions(mixed, S, dtype="f32", layout="nchw").cpu()
