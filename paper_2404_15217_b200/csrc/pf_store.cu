@@ -507,6 +507,41 @@ __device__ __forceinline__ void passthrough_out(const uint8_t* work, int row_byt
         if constexpr (kLdg) return __ldg(lut + i);
         else return lut[i];
     };
+#ifndef PF_PT_ITEM_CH
+    if constexpr (kLdg) {
+        // lean kernel: one item = 4 pixels x 3 channels; its 12 staged bytes are read as 4
+        // aligned words and funnel-shifted (4 LDS instead of 12 byte loads), then one 4-wide
+        // store per channel plane.  The staged band has >= 16 B of slack after its last row
+        // (host smem size), so the 4th word is always inside the allocation.
+        if (lay == PF_NCHW && (S % 4) == 0) {
+            const int G = S / 4;
+            for (int q = threadIdx.x; q < nr * G; q += blockDim.x) {
+                const int rr = q / G, x0 = (q - rr * G) * 4;
+                const int off = rr * row_bytes + base + x0 * 3;
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(work + (off & ~3));
+                const uint32_t a0 = w[0], a1 = w[1], a2 = w[2], a3 = w[3];
+                const uint32_t sh = (uint32_t)(off & 3) * 8;
+                const uint32_t b[3] = {__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh),
+                                       __funnelshift_r(a2, a3, sh)};
+                OT* dst = o + (size_t)(y0 + rr) * S + x0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    OT v[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int j = 3 * k + c;  // byte j of the 12: pixel k, channel c
+                        v[k] = L(c * 256 + (int)((b[j >> 2] >> ((j & 3) * 8)) & 0xffu));
+                    }
+                    OT* d = dst + c * plane;
+                    if constexpr (sizeof(OT) == 4) *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(v);
+                    else if constexpr (sizeof(OT) == 2) *reinterpret_cast<uint2*>(d) = *reinterpret_cast<const uint2*>(v);
+                    else *reinterpret_cast<uint32_t*>(d) = *reinterpret_cast<const uint32_t*>(v);
+                }
+            }
+            return;
+        }
+    }
+#endif
     if (lay == PF_NCHW && (S % 4) == 0) {
         const int G = S / 4;
         for (int q = threadIdx.x; q < 3 * nr * G; q += blockDim.x) {
