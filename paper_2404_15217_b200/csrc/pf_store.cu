@@ -763,7 +763,8 @@ __global__ void __launch_bounds__(kRRThreads) read_regions_kernel(const pf_slide
 // table through L1 instead of 768 divided entries built per CTA.  28-row bands (8 per 224 px
 // patch: 2048 CTAs for C1's 256 patches, ~19 KB so still 8 CTAs per SM) measured 4 % faster than
 // 16 (C1 4.04 -> 4.21 M patches/s); 12, 20, 24 and 32 rows no better than 16, and 32 rows exceed
-// the 48 KB default dynamic shared memory at out_size 512.  Streaming (.cs) stores: neutral.  A
+// the 48 KB default dynamic shared memory at out_size 512.  Streaming (.cs) stores, and 6 or 8
+// CTAs per SM forced by __launch_bounds__ (5 at 48 registers): neutral.  A
 // persistent grid double-buffering the next band's rows was no faster.
 #ifndef PF_PT_BAND
 #define PF_PT_BAND 28
